@@ -1,0 +1,215 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes bindings to the parity checkers.
+
+* ``liboracle.so``   -- C restatement of the reference column physics
+  (oracle/convproxy_oracle.c, each function cites physics.cpp lines).
+* ``_ref/libconvref.so`` -- the reference's own physics.cpp/sched.cpp compiled
+  in place from /root/reference by oracle/Makefile (absent if the build
+  container had no reference tree).
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline /
+``--impl reference`` leg may import this package.  The product path
+(paper_1711_00289_b200) never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libconvref.so")
+
+EXACT, STRENGTH_REDUCED, APPROX_TRANSCENDENTAL = 0, 1, 2
+FAIL_NAMES = {0: "ok", 1: "non-finite activity", 2: "non-finite input",
+              3: "iterate diverged", 4: "no convergence"}
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+
+
+class Options(C.Structure):
+    """Mirrors convproxy::KernelOptions (physics.hpp:68-73)."""
+    _fields_ = [("variant", C.c_int), ("activity_threshold", C.c_double),
+                ("newton_tol", C.c_double), ("newton_max_iter", C.c_int)]
+
+    def __init__(self, variant=EXACT, activity_threshold=0.5, newton_tol=1e-12,
+                 newton_max_iter=100):
+        super().__init__(variant, activity_threshold, newton_tol, newton_max_iter)
+
+
+_orc = None
+_ref = None
+
+
+def lib():
+    global _orc
+    if _orc is None:
+        if not os.path.exists(ORACLE_SO):
+            raise RuntimeError(f"oracle library missing: {ORACLE_SO} (run make -C oracle)")
+        L = C.CDLL(ORACLE_SO)
+        L.orc_rng_u64.restype = C.c_uint64
+        L.orc_rng_u64.argtypes = [C.c_uint64] * 3
+        L.orc_rng_u01.restype = C.c_double
+        L.orc_rng_u01.argtypes = [C.c_uint64] * 3
+        L.orc_approx_exp.restype = C.c_double
+        L.orc_approx_exp.argtypes = [C.c_double]
+        L.orc_ientropy_solve.restype = C.c_int
+        L.orc_ientropy_solve.argtypes = [C.c_double, C.c_double, C.POINTER(Options),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                         C.POINTER(C.c_double)]
+        for name in ("orc_deep_convection", "orc_shallow_convection"):
+            f = getattr(L, name)
+            f.restype = C.c_int
+            f.argtypes = [C.c_longlong, C.c_int, C.c_longlong, C.c_longlong,
+                          _dp, _dp, _dp, C.POINTER(Options), _dp, _dp, _dp, _i64p,
+                          _u8p, _dp, C.POINTER(C.c_longlong)]
+        L.orc_make_grid.restype = None
+        L.orc_make_grid.argtypes = [C.c_longlong, C.c_int, C.c_double, C.c_uint64,
+                                    _dp, _dp, _dp]
+        _orc = L
+    return _orc
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            raise RuntimeError(f"reference build missing: {REF_SO}")
+        L = C.CDLL(REF_SO)
+        L.ref_convection.restype = C.c_int
+        L.ref_convection.argtypes = [C.c_int, C.c_longlong, C.c_int, C.c_longlong,
+                                     C.c_longlong, _dp, _dp, _dp, C.c_int, C.c_double,
+                                     C.c_double, C.c_int, _dp, _dp, _dp, _i64p, _u8p,
+                                     C.POINTER(C.c_longlong)]
+        L.ref_ientropy_solve.restype = C.c_int
+        L.ref_ientropy_solve.argtypes = [C.c_double, C.c_double, C.c_int, C.c_double,
+                                         C.c_int, C.POINTER(C.c_double),
+                                         C.POINTER(C.c_int)]
+        L.ref_approx_exp.restype = C.c_double
+        L.ref_approx_exp.argtypes = [C.c_double]
+        L.ref_make_grid.restype = None
+        L.ref_make_grid.argtypes = [C.c_longlong, C.c_int, C.c_double, C.c_ulonglong,
+                                    _dp, _dp, _dp]
+        L.ref_chunk_create.restype = C.c_void_p
+        L.ref_chunk_create.argtypes = [C.c_longlong, C.c_int, C.c_longlong,
+                                       C.c_longlong, _dp, _dp, _dp]
+        L.ref_chunk_free.restype = None
+        L.ref_chunk_free.argtypes = [C.c_void_p]
+        L.ref_run_parallel.restype = C.c_int
+        L.ref_run_parallel.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double,
+                                       C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.POINTER(C.c_double), C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]
+        _ref = L
+    return _ref
+
+
+class Result:
+    """SoA outputs of one kernel pass (level-major [L][n])."""
+
+    def __init__(self, n, L):
+        self.tend_T = np.zeros((L, n))
+        self.tend_q = np.zeros((L, n))
+        self.precip = np.zeros(n)
+        self.work = np.zeros(n, dtype=np.int64)
+        self.exited = np.zeros(n, dtype=np.uint8)
+        self.margin = np.full(n, np.inf)
+        self.status = 0
+        self.fail_col = -1
+
+
+def _soa(s, T, q):
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    assert T.shape == q.shape and T.shape[1] == s.shape[0]
+    return s, T, q
+
+
+def convection(kernel: str, s, T, q, opts: Options | None = None, first_col=0) -> Result:
+    """Oracle pass: kernel in {"deep", "shallow"}; returns Result (with the
+    Newton / predicate margin diagnostics in ``margin``)."""
+    opts = opts or Options()
+    s, T, q = _soa(s, T, q)
+    L, n = T.shape
+    r = Result(n, L)
+    fc = C.c_longlong(-1)
+    f = lib().orc_deep_convection if kernel == "deep" else lib().orc_shallow_convection
+    r.status = f(n, L, n, first_col, s, T, q, C.byref(opts), r.tend_T, r.tend_q,
+                 r.precip, r.work, r.exited, r.margin, C.byref(fc))
+    r.fail_col = fc.value
+    return r
+
+
+def ref_convection(kernel: str, s, T, q, opts: Options | None = None, first_col=0) -> Result:
+    """The reference's own deep_convection/shallow_convection (physics.hpp:155-158)."""
+    opts = opts or Options()
+    s, T, q = _soa(s, T, q)
+    L, n = T.shape
+    r = Result(n, L)
+    fc = C.c_longlong(-1)
+    r.status = ref_lib().ref_convection(0 if kernel == "deep" else 1, n, L, n, first_col,
+                                        s, T, q, opts.variant, opts.activity_threshold,
+                                        opts.newton_tol, opts.newton_max_iter, r.tend_T,
+                                        r.tend_q, r.precip, r.work, r.exited, C.byref(fc))
+    r.fail_col = fc.value
+    return r
+
+
+def ientropy_solve(y, guess, opts: Options | None = None):
+    opts = opts or Options()
+    root, it, mm = C.c_double(), C.c_int(), C.c_double()
+    st = lib().orc_ientropy_solve(y, guess, C.byref(opts), C.byref(root), C.byref(it),
+                                  C.byref(mm))
+    return st, root.value, it.value, mm.value
+
+
+def make_grid(n, L=30, tropics_band=0.3, seed=42):
+    s = np.empty(n)
+    T = np.empty((L, n))
+    q = np.empty((L, n))
+    lib().orc_make_grid(n, L, tropics_band, seed, s, T, q)
+    return s, T, q
+
+
+def ref_make_grid(n, L=30, tropics_band=0.3, seed=42):
+    s = np.empty(n)
+    T = np.empty((L, n))
+    q = np.empty((L, n))
+    ref_lib().ref_make_grid(n, L, tropics_band, seed, s, T, q)
+    return s, T, q
+
+
+def ref_time_run_parallel(s, T, q, opts: Options | None = None, n_threads=None,
+                          strategy=2, omp_chunk=1, kernels=("deep", "shallow")):
+    """Wall seconds of the reference run_parallel over the sample, one entry
+    per kernel (reference RunMetrics::wall_s, sched.cpp:196-201)."""
+    opts = opts or Options()
+    s, T, q = _soa(s, T, q)
+    L, n = T.shape
+    n_threads = n_threads or os.cpu_count() or 1
+    R = ref_lib()
+    h = R.ref_chunk_create(n, L, n, 0, s, T, q)
+    if not h:
+        raise RuntimeError("ref_chunk_create failed")
+    try:
+        out = {}
+        for k in kernels:
+            w = C.c_double()
+            st = R.ref_run_parallel(h, 0 if k == "deep" else 1, opts.variant,
+                                    opts.activity_threshold, opts.newton_tol,
+                                    opts.newton_max_iter, n_threads, strategy, omp_chunk,
+                                    C.byref(w), None, None, None, None, None)
+            if st != 0:
+                raise RuntimeError(f"reference run_parallel failed ({st})")
+            out[k] = w.value
+        return out
+    finally:
+        R.ref_chunk_free(h)
