@@ -1,0 +1,178 @@
+/*
+ * convgpu.h -- C ABI of the B200 (sm_100a) deep + shallow convection column
+ * path.  Drop-in for the reference's column-batch entry points:
+ *
+ *   std::vector<ColumnOutput> deep_convection(const Chunk&, const KernelOptions&)
+ *   std::vector<ColumnOutput> shallow_convection(const Chunk&, const KernelOptions&)
+ *       /root/reference/proj/src/core/physics.hpp:155-158
+ *   IentropyResult ientropy_solve(double y, double guess, const KernelOptions&)
+ *       physics.hpp:101 (physics.cpp:101-104)
+ *   double approx_exp(double x)                        physics.hpp:83
+ *
+ * Conventions follow the reference C API (proj/include/convproxy.h:34-41,
+ * proj/src/capi.cpp:39-89): every call returns a cvg_status with the same
+ * numeric codes as cvp_status; on failure cvg_last_error() holds a
+ * thread-local message, cleared by the next successful call; null arguments
+ * give CVG_ERR_INVALID with "null" in the message; no C++ exception crosses
+ * this boundary.  A kernel failure (KernelError in the reference,
+ * errors.hpp:26-36) returns CVG_ERR_NUMERIC, names the LOWEST failing column
+ * ("... column <id>") -- the column the serial driver physics.cpp:227-245
+ * would have thrown on -- and stores it in cvg_stats.failing_column.
+ *
+ * Data layout: level-major structure of arrays.  Field f of level k, column c
+ * lives at f[k * ld + c] (ld >= n_columns); per-column scalars are f[c].
+ * Pointers may be host or device memory (cvg_columns.on_device); the caller
+ * owns every buffer; inputs are never modified.  The library owns only its
+ * per-context device workspace and streams.
+ *
+ * One call in flight per context; contexts are independent (one per device /
+ * per rank).  All pointers and sizes are plain C types.
+ */
+#ifndef CONVGPU_H_
+#define CONVGPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum cvg_status {
+  CVG_OK = 0,
+  CVG_ERR_INVALID = 1, /* null handle, bad argument, internal failure      */
+  CVG_ERR_CONFIG = 2,  /* (reserved; same code as CVP_ERR_CONFIG)          */
+  CVG_ERR_NUMERIC = 3, /* kernel numeric failure: NaN, divergence, maxiter  */
+  CVG_ERR_CHECK = 4,   /* (reserved; same code as CVP_ERR_CHECK)           */
+  CVG_ERR_IO = 5,      /* (reserved; same code as CVP_ERR_IO)              */
+  CVG_ERR_DEVICE = 6   /* CUDA runtime failure or no usable sm_100 device  */
+} cvg_status;
+
+/* convproxy::Variant, physics.hpp:62-66 */
+typedef enum cvg_variant {
+  CVG_EXACT = 0,
+  CVG_STRENGTH_REDUCED = 1,
+  CVG_APPROX_TRANSCENDENTAL = 2
+} cvg_variant;
+
+/* Which kernels one cvg_convect call runs. */
+enum { CVG_DEEP = 1, CVG_SHALLOW = 2, CVG_BOTH = 3 };
+
+/* Failure kinds reported in cvg_stats.failure_kind (reference messages in
+ * physics.cpp:67, :79, :84-85, :109, :172). */
+enum {
+  CVG_FAIL_NONE = 0,
+  CVG_FAIL_ACTIVITY = 1, /* non-finite activity s           */
+  CVG_FAIL_INPUT = 2,    /* ientropy: non-finite input      */
+  CVG_FAIL_DIVERGED = 3, /* ientropy: iterate diverged      */
+  CVG_FAIL_NOCONV = 4    /* ientropy: no convergence        */
+};
+
+/* convproxy::KernelOptions, physics.hpp:68-73 (same defaults). */
+typedef struct cvg_options {
+  int variant;               /* cvg_variant, default CVG_EXACT   */
+  double activity_threshold; /* default 0.5                       */
+  double newton_tol;         /* default 1e-12 (absolute)          */
+  int newton_max_iter;       /* default 100                       */
+} cvg_options;
+
+/* Input column block (the SoA form of convproxy::Chunk, physics.hpp:39-43). */
+typedef struct cvg_columns {
+  long long n_columns;
+  int n_levels;
+  long long first_col; /* column id of column 0 (ColumnState::col_id)     */
+  long long ld;        /* row stride of T and q in elements (>= n_columns) */
+  const double* s;     /* [n]        activity                              */
+  const double* T;     /* [L][ld]    temperature-like field                */
+  const double* q;     /* [L][ld]    moisture-like field                   */
+  int on_device;       /* 1: pointers are device memory on the ctx device */
+} cvg_columns;
+
+/* Output block (the SoA form of std::vector<ColumnOutput>, physics.hpp:52-60). */
+typedef struct cvg_outputs {
+  double* tend_T;         /* [L][ld] */
+  double* tend_q;         /* [L][ld] */
+  double* precip;         /* [n]     */
+  long long* work_units;  /* [n]     */
+  uint8_t* exited_early;  /* [n]     */
+  long long ld;           /* row stride of tend_T / tend_q (>= n_columns) */
+  int on_device;
+} cvg_outputs;
+
+typedef struct cvg_stats {
+  long long n_columns;
+  long long n_triggered;     /* deep columns with s > activity_threshold      */
+  long long failing_column;  /* lowest failing column id, or -1              */
+  int failure_kind;          /* CVG_FAIL_*                                    */
+  int failing_kernel;        /* CVG_DEEP / CVG_SHALLOW, 0 when none          */
+  double device_ms;          /* device time of the compute (CUDA events)      */
+  double h2d_ms, d2h_ms;     /* staging copies (host buffers only)           */
+  long long h2d_bytes, d2h_bytes;
+} cvg_stats;
+
+typedef struct cvg_context cvg_context;
+
+const char* cvg_version(void);
+const char* cvg_last_error(void);
+void cvg_default_options(cvg_options* opts);
+
+/* Creates a context on CUDA device `device` (requires compute capability 10.x). */
+cvg_status cvg_context_create(int device, cvg_context** out);
+void cvg_context_free(cvg_context* ctx);
+
+/* Runs deep and/or shallow convection (kernel_mask) over one column block.
+ * deep / shallow may be NULL when not requested.  Host buffers are staged
+ * through pinned device workspace; device buffers are used in place.  On
+ * return all outputs are complete (the call synchronises its stream).
+ * stats may be NULL. */
+cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in,
+                       const cvg_options* opts, int kernel_mask,
+                       const cvg_outputs* deep, const cvg_outputs* shallow,
+                       cvg_stats* stats);
+
+/* Asynchronous device-resident form for steady-state loops and CUDA-graph
+ * capture: all pointers must be device memory; work is enqueued on `stream`
+ * (a cudaStream_t, NULL = the context stream) and errors are latched on the
+ * device.  cvg_convect_check() synchronises that stream, reads the latched
+ * error, fills stats and clears it. */
+cvg_status cvg_convect_async(cvg_context* ctx, const cvg_columns* in,
+                             const cvg_options* opts, int kernel_mask,
+                             const cvg_outputs* deep,
+                             const cvg_outputs* shallow, void* stream);
+cvg_status cvg_convect_check(cvg_context* ctx, void* stream, cvg_stats* stats);
+
+/* Reference batch entry points (physics.hpp:155-158) over HOST SoA buffers. */
+cvg_status cvg_deep_convection(cvg_context* ctx, const cvg_columns* in,
+                               const cvg_options* opts, const cvg_outputs* out,
+                               cvg_stats* stats);
+cvg_status cvg_shallow_convection(cvg_context* ctx, const cvg_columns* in,
+                                  const cvg_options* opts,
+                                  const cvg_outputs* out, cvg_stats* stats);
+
+/* Batched inverse-entropy solve on the device (physics.hpp:101): n
+ * independent (y, guess) pairs -> root, iterations.  On failure returns
+ * CVG_ERR_NUMERIC with the lowest failing index in the message. */
+cvg_status cvg_ientropy_solve(cvg_context* ctx, long long n, const double* y,
+                              const double* guess, const cvg_options* opts,
+                              double* root, int* iterations);
+
+/* Device evaluation of approx_exp (physics.hpp:83) over n host values. */
+cvg_status cvg_approx_exp(cvg_context* ctx, long long n, const double* x,
+                          double* out);
+
+/* Host-side partition of a column block across n_parts devices, balanced by
+ * estimated cost w_c = deep_weight * [s_c > thr] + shallow_weight
+ * (generalises plan_partition, hetero.cpp:156-176, from a 2-pool split to
+ * G contiguous ranges).  bounds receives n_parts + 1 offsets, bounds[0] = 0,
+ * bounds[n_parts] = n.  deep_weight <= 0 selects the naive equal-columns
+ * split (the analogue of StaticBlock, sched.cpp:66-75). */
+cvg_status cvg_plan_partition(long long n, const double* s,
+                              double activity_threshold, int n_parts,
+                              double deep_weight, double shallow_weight,
+                              long long* bounds);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* CONVGPU_H_ */

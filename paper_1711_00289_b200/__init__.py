@@ -1,0 +1,322 @@
+"""B200-native (sm_100a) deep + shallow convection column path.
+
+Python mirror of the reference's column-batch interface over the C ABI in
+``include/convgpu.h`` (``libconvgpu.so``, built from ``csrc/``):
+
+* ``deep_convection`` / ``shallow_convection``  <- physics.hpp:155-158
+* ``ientropy_solve``                            <- physics.hpp:101
+* ``approx_exp``                                <- physics.hpp:83
+* ``KernelOptions`` / ``Variant``               <- physics.hpp:62-73
+* ``KernelError`` (column id)                   <- errors.hpp:26-36
+* ``plan_partition`` (G-way, count-balanced)    <- hetero.cpp:156-176
+
+Columns travel as level-major structure-of-arrays: ``s[n]``, ``T[L][n]``,
+``q[L][n]``.  There is no CPU fallback: if the CUDA library is missing or no
+sm_100 device is present, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "Variant", "KernelOptions", "KernelError", "DeviceError", "ColumnOutputs", "Stats",
+    "Context", "deep_convection", "shallow_convection", "ientropy_solve", "approx_exp",
+    "plan_partition", "library_path", "load_library", "DEEP", "SHALLOW", "BOTH",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_NAME = "libconvgpu.so"
+DEEP, SHALLOW, BOTH = 1, 2, 3
+
+
+class Variant:
+    """convproxy::Variant (physics.hpp:62-66)."""
+    EXACT = 0
+    STRENGTH_REDUCED = 1
+    APPROX_TRANSCENDENTAL = 2
+
+
+class KernelOptions(C.Structure):
+    """convproxy::KernelOptions (physics.hpp:68-73), same defaults."""
+    _fields_ = [("variant", C.c_int), ("activity_threshold", C.c_double),
+                ("newton_tol", C.c_double), ("newton_max_iter", C.c_int)]
+
+    def __init__(self, variant=Variant.EXACT, activity_threshold=0.5, newton_tol=1e-12,
+                 newton_max_iter=100):
+        super().__init__(int(variant), float(activity_threshold), float(newton_tol),
+                         int(newton_max_iter))
+
+    def __repr__(self):
+        return (f"KernelOptions(variant={self.variant}, activity_threshold={self.activity_threshold},"
+                f" newton_tol={self.newton_tol}, newton_max_iter={self.newton_max_iter})")
+
+
+class _Columns(C.Structure):
+    _fields_ = [("n_columns", C.c_longlong), ("n_levels", C.c_int), ("first_col", C.c_longlong),
+                ("ld", C.c_longlong), ("s", C.c_void_p), ("T", C.c_void_p), ("q", C.c_void_p),
+                ("on_device", C.c_int)]
+
+
+class _Outputs(C.Structure):
+    _fields_ = [("tend_T", C.c_void_p), ("tend_q", C.c_void_p), ("precip", C.c_void_p),
+                ("work_units", C.c_void_p), ("exited_early", C.c_void_p), ("ld", C.c_longlong),
+                ("on_device", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("n_columns", C.c_longlong), ("n_triggered", C.c_longlong),
+                ("failing_column", C.c_longlong), ("failure_kind", C.c_int),
+                ("failing_kernel", C.c_int), ("device_ms", C.c_double), ("h2d_ms", C.c_double),
+                ("d2h_ms", C.c_double), ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong)]
+
+
+CVG_OK, CVG_ERR_INVALID, CVG_ERR_NUMERIC, CVG_ERR_DEVICE = 0, 1, 3, 6
+
+
+class KernelError(RuntimeError):
+    """Numeric failure in a column kernel; ``column`` is the lowest failing
+    column id (what the serial reference would have thrown on)."""
+
+    def __init__(self, msg, column=-1, kind=0):
+        super().__init__(msg)
+        self.column = column
+        self.kind = kind
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+def library_path() -> str:
+    return os.environ.get("CONVGPU_LIB", os.path.join(HERE, LIB_NAME))
+
+
+_lib = None
+
+
+def load_library():
+    """Loads libconvgpu.so; raises (no fallback) if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = library_path()
+    if not os.path.exists(path):
+        raise DeviceError(f"CUDA library {path} is missing; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    vp, i64, i32, dbl = C.c_void_p, C.c_longlong, C.c_int, C.c_double
+    L.cvg_version.restype = C.c_char_p
+    L.cvg_last_error.restype = C.c_char_p
+    L.cvg_default_options.argtypes = [C.POINTER(KernelOptions)]
+    L.cvg_context_create.argtypes = [i32, C.POINTER(vp)]
+    L.cvg_context_free.argtypes = [vp]
+    L.cvg_context_free.restype = None
+    L.cvg_convect.argtypes = [vp, C.POINTER(_Columns), C.POINTER(KernelOptions), i32,
+                              C.POINTER(_Outputs), C.POINTER(_Outputs), C.POINTER(Stats)]
+    L.cvg_convect_async.argtypes = [vp, C.POINTER(_Columns), C.POINTER(KernelOptions), i32,
+                                    C.POINTER(_Outputs), C.POINTER(_Outputs), vp]
+    L.cvg_convect_check.argtypes = [vp, vp, C.POINTER(Stats)]
+    L.cvg_deep_convection.argtypes = [vp, C.POINTER(_Columns), C.POINTER(KernelOptions),
+                                      C.POINTER(_Outputs), C.POINTER(Stats)]
+    L.cvg_shallow_convection.argtypes = L.cvg_deep_convection.argtypes
+    L.cvg_ientropy_solve.argtypes = [vp, i64, vp, vp, C.POINTER(KernelOptions), vp, vp]
+    L.cvg_approx_exp.argtypes = [vp, i64, vp, vp]
+    L.cvg_plan_partition.argtypes = [i64, vp, dbl, i32, dbl, dbl, vp]
+    for f in ("cvg_context_create", "cvg_convect", "cvg_convect_async", "cvg_convect_check",
+              "cvg_deep_convection", "cvg_shallow_convection", "cvg_ientropy_solve",
+              "cvg_approx_exp", "cvg_plan_partition"):
+        getattr(L, f).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _raise(rc, stats: Stats | None = None):
+    if rc == CVG_OK:
+        return
+    msg = load_library().cvg_last_error().decode()
+    if rc == CVG_ERR_NUMERIC:
+        col = stats.failing_column if stats is not None else -1
+        kind = stats.failure_kind if stats is not None else 0
+        raise KernelError(msg, col, kind)
+    if rc == CVG_ERR_DEVICE:
+        raise DeviceError(msg)
+    raise ValueError(f"convgpu status {rc}: {msg}")
+
+
+@dataclass
+class ColumnOutputs:
+    """SoA form of std::vector<ColumnOutput> (physics.hpp:52-60)."""
+    tend_T: np.ndarray   # [L][n]
+    tend_q: np.ndarray   # [L][n]
+    precip: np.ndarray   # [n]
+    work_units: np.ndarray  # [n] int64
+    exited_early: np.ndarray  # [n] uint8
+
+    @classmethod
+    def empty(cls, n, L):
+        return cls(np.empty((L, n)), np.empty((L, n)), np.empty(n), np.empty(n, np.int64),
+                   np.empty(n, np.uint8))
+
+    def _struct(self):
+        return _Outputs(self.tend_T.ctypes.data, self.tend_q.ctypes.data, self.precip.ctypes.data,
+                        self.work_units.ctypes.data, self.exited_early.ctypes.data,
+                        self.tend_T.shape[1] if self.tend_T.ndim == 2 else 0, 0)
+
+
+def _host_columns(s, T, q, first_col):
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    if T.ndim != 2 or T.shape != q.shape or T.shape[1] != s.shape[0]:
+        raise ValueError("expected s[n], T[L][n], q[L][n]")
+    L, n = T.shape
+    return (s, T, q), _Columns(n, L, first_col, n, s.ctypes.data, T.ctypes.data, q.ctypes.data, 0)
+
+
+class Context:
+    """One device context (cvg_context): persistent workspace, one call in
+    flight.  Use one per GPU / per rank."""
+
+    def __init__(self, device: int = 0):
+        L = load_library()
+        h = C.c_void_p()
+        _raise(L.cvg_context_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+        self.last_stats = Stats()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().cvg_context_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- host (numpy) entry points -------------------------------------------
+    def convect(self, s, T, q, opts: KernelOptions | None = None, kernels=BOTH, first_col=0):
+        """Runs deep and/or shallow over host SoA arrays; returns (deep, shallow)
+        ColumnOutputs (None for a kernel not requested)."""
+        opts = opts or KernelOptions()
+        keep, cols = _host_columns(s, T, q, first_col)
+        L, n = keep[1].shape
+        deep = ColumnOutputs.empty(n, L) if kernels & DEEP else None
+        sh = ColumnOutputs.empty(n, L) if kernels & SHALLOW else None
+        st = Stats()
+        rc = load_library().cvg_convect(self._h, C.byref(cols), C.byref(opts), kernels,
+                                        C.byref(deep._struct()) if deep else None,
+                                        C.byref(sh._struct()) if sh else None, C.byref(st))
+        self.last_stats = st
+        _raise(rc, st)
+        return deep, sh
+
+    def deep_convection(self, s, T, q, opts=None, first_col=0) -> ColumnOutputs:
+        return self.convect(s, T, q, opts, DEEP, first_col)[0]
+
+    def shallow_convection(self, s, T, q, opts=None, first_col=0) -> ColumnOutputs:
+        return self.convect(s, T, q, opts, SHALLOW, first_col)[1]
+
+    def ientropy_solve(self, y, guess, opts: KernelOptions | None = None):
+        opts = opts or KernelOptions()
+        y = np.ascontiguousarray(np.atleast_1d(y), dtype=np.float64)
+        g = np.ascontiguousarray(np.broadcast_to(np.asarray(guess, dtype=np.float64), y.shape))
+        root = np.empty_like(y)
+        it = np.empty(y.shape, dtype=np.int32)
+        rc = load_library().cvg_ientropy_solve(self._h, y.size, y.ctypes.data, g.ctypes.data,
+                                               C.byref(opts), root.ctypes.data, it.ctypes.data)
+        _raise(rc)
+        return root, it
+
+    def approx_exp(self, x):
+        x = np.ascontiguousarray(np.atleast_1d(x), dtype=np.float64)
+        out = np.empty_like(x)
+        _raise(load_library().cvg_approx_exp(self._h, x.size, x.ctypes.data, out.ctypes.data))
+        return out
+
+    # -- device-resident entry points (torch CUDA tensors or raw pointers) ----
+    def convect_async(self, s, T, q, deep, shallow, opts: KernelOptions | None = None,
+                      kernels=BOTH, first_col=0, stream=None):
+        """Enqueues on `stream` (a torch.cuda.Stream, raw handle or None for the
+        context stream).  s/T/q and the output tuples are CUDA tensors
+        (tend_T, tend_q, precip, work, exited)."""
+        opts = opts or KernelOptions()
+        n = s.numel()
+        L = T.shape[0]
+        cols = _Columns(n, L, first_col, T.stride(0), s.data_ptr(), T.data_ptr(), q.data_ptr(), 1)
+
+        def outs(o):
+            if o is None:
+                return None
+            tT, tq, pr, wk, ex = o
+            return C.byref(_Outputs(tT.data_ptr(), tq.data_ptr(), pr.data_ptr(), wk.data_ptr(),
+                                    ex.data_ptr(), tT.stride(0), 1))
+
+        h = None
+        if stream is not None:
+            h = getattr(stream, "cuda_stream", stream)
+        rc = load_library().cvg_convect_async(self._h, C.byref(cols), C.byref(opts), kernels,
+                                              outs(deep), outs(shallow), h)
+        _raise(rc)
+
+    def check(self, stream=None) -> Stats:
+        st = Stats()
+        h = None if stream is None else getattr(stream, "cuda_stream", stream)
+        rc = load_library().cvg_convect_check(self._h, h, C.byref(st))
+        self.last_stats = st
+        _raise(rc, st)
+        return st
+
+
+_default_ctx: Context | None = None
+
+
+def _ctx() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def deep_convection(s, T, q, opts=None, first_col=0) -> ColumnOutputs:
+    """physics.hpp:155 -- deep convection over a column block on the GPU."""
+    return _ctx().deep_convection(s, T, q, opts, first_col)
+
+
+def shallow_convection(s, T, q, opts=None, first_col=0) -> ColumnOutputs:
+    """physics.hpp:157 -- shallow convection over a column block on the GPU."""
+    return _ctx().shallow_convection(s, T, q, opts, first_col)
+
+
+def ientropy_solve(y, guess, opts=None):
+    """physics.hpp:101 -- batched on the GPU; returns (root, iterations)."""
+    return _ctx().ientropy_solve(y, guess, opts)
+
+
+def approx_exp(x):
+    """physics.hpp:83 -- evaluated on the GPU."""
+    return _ctx().approx_exp(x)
+
+
+def plan_partition(s, activity_threshold: float, n_parts: int, deep_weight: float = 1.0,
+                   shallow_weight: float = 0.0) -> np.ndarray:
+    """Contiguous G-way column split balanced by estimated cost (host C++,
+    cvg_plan_partition).  deep_weight <= 0 gives the naive equal split."""
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    b = np.empty(n_parts + 1, dtype=np.int64)
+    rc = load_library().cvg_plan_partition(s.size, s.ctypes.data, float(activity_threshold),
+                                           int(n_parts), float(deep_weight), float(shallow_weight),
+                                           b.ctypes.data)
+    _raise(rc)
+    return b
