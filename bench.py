@@ -1,0 +1,449 @@
+#!/usr/bin/env python3
+"""Benchmark: convective columns/s (deep + shallow, fp64) on B200.
+
+One step = one pass of the hot path (trigger + compaction, deep plume,
+shallow + deep zero-fill) over the whole column block, inputs resident in
+HBM.  At N GPUs (torchrun, one rank per GPU) the f02 grid is partitioned into
+N contiguous ranges balanced by estimated cost (cvg_plan_partition); there is
+no collective on the data path -- torch.distributed/NCCL is used only for the
+barrier and the max-over-ranks of the device timings.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's own
+CPU implementation (oracle/_ref: physics.cpp + sched.cpp compiled from the
+reference sources, run through its run_parallel dynamic scheduler on all host
+threads) on the same workload and prints the same line with impl=reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "convective columns/sec (deep+shallow, fp64)"
+UNIT = "columns/s"
+HBM_FALLBACK_GBS = 6650.0
+L2_BYTES = 126 * 2 ** 20
+
+
+# ---------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def init_dist(ws, backend):
+    if ws <= 1:
+        return None
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group(backend=backend)
+    return dist
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# FLOP / byte model; per-column integers come from the
+# step's own outputs (work_units, exited_early), which match the oracle's.
+def flop_model(L, deep_work, deep_exited, sh_work, sh_exited):
+    trig = deep_exited == 0
+    U = deep_work[trig].astype(np.float64)
+    deep_flops = float(np.sum(159.0 * L + 37.0 * U))
+    P = (sh_work // L).astype(np.float64)
+    surv = (sh_exited == 0)
+    sh_flops = float(np.sum(P * (9 * L + 8 + 29) + (P >= 2) * L * (3 + 29) + surv * (6 * L + 3 + 29)))
+    return deep_flops, sh_flops, int(trig.sum())
+
+
+def bytes_model(n, L, n_trig):
+    per_col = 8 + 2 * 8 * L + 2 * (2 * 8 * L + 8 + 8 + 1)   # 1,482 B at L = 30
+    deep_only = n_trig * (8 + 2 * 8 * L + 2 * 8 * L + 8 + 8 + 1)
+    return n * per_col, per_col, deep_only
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        if not self._nv:
+            return None
+        r = [name for bit, name in self.REASONS.items() if self.reasons & bit and name != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": r, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_time(s, T, q, thr, threads, variant=0, reps=3, warm=1):
+    """Reference run_parallel (Dynamic, omp_chunk 1) deep + shallow wall time,
+    median of `reps` after `warm` warm-ups."""
+    import oracle as O
+    opts = O.Options(variant=variant, activity_threshold=thr)
+    walls = []
+    for i in range(warm + reps):
+        w = O.ref_time_run_parallel(s, T, q, opts, n_threads=threads, strategy=2, omp_chunk=1)
+        if i >= warm:
+            walls.append(w["deep"] + w["shallow"])
+    return float(np.median(walls))
+
+
+def cpu_port_time(s, T, q, thr, variant=0):
+    import oracle as O
+    opts = O.Options(variant=variant, activity_threshold=thr)
+    t0 = time.perf_counter()
+    O.convection("deep", s, T, q, opts)
+    O.convection("shallow", s, T, q, opts)
+    return time.perf_counter() - t0
+
+
+def strided_sample(s, T, q, stride):
+    idx = np.arange(0, s.size, stride)
+    return np.ascontiguousarray(s[idx]), np.ascontiguousarray(T[:, idx]), np.ascontiguousarray(q[:, idx])
+
+
+def cpu_baseline(s, T, q, thr, variant, target_s=10.0):
+    """Bounded sample of the workload on the host cores (rank 0, N=1)."""
+    import oracle as O
+    threads = os.cpu_count() or 1
+    if O.ref_available():
+        # calibrate on a small strided sample, then size the sample so one
+        # timed rep is ~target_s / 4 seconds of wall
+        cal_stride = max(1, s.size // 20000)
+        cs, cT, cq = strided_sample(s, T, q, cal_stride)
+        t = cpu_reference_time(cs, cT, cq, thr, threads, variant, reps=1, warm=0)
+        rate = cs.size / max(t, 1e-6)
+        want = int(min(s.size, max(2000, rate * target_s / 4)))
+        stride = max(1, s.size // want)
+        ss, sT, sq = strided_sample(s, T, q, stride)
+        wall = cpu_reference_time(ss, sT, sq, thr, threads, variant, reps=3, warm=1)
+        return {"value": ss.size / wall, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"every {stride}th column of the same grid ({ss.size} columns), reference "
+                          f"run_parallel Dynamic(omp_chunk=1) deep+shallow, median of 3 after 1 warm-up",
+                "wall_s": wall}
+    stride = max(1, s.size // 20000)
+    ss, sT, sq = strided_sample(s, T, q, stride)
+    wall = cpu_port_time(ss, sT, sq, thr, variant)
+    return {"value": ss.size / wall, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"every {stride}th column ({ss.size} columns), serial C oracle", "wall_s": wall}
+
+
+# ---------------------------------------------------------------------------
+def run_reference_arm(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1711_00289_b200 import gridgen
+    import oracle as O
+    thr = gridgen.config_threshold(args.config)
+    s, T, q = gridgen.make_config(args.config, seed=args.seed)
+    threads = os.cpu_count() or 1
+    kind = "reference" if O.ref_available() else "port"
+    # size one step's sample to ~1.5 s of wall so K+W steps stay within minutes
+    cal_stride = max(1, s.size // 20000)
+    cs, cT, cq = strided_sample(s, T, q, cal_stride)
+    if kind == "reference":
+        t = cpu_reference_time(cs, cT, cq, thr, threads, args.variant, reps=1, warm=0)
+    else:
+        t = cpu_port_time(cs, cT, cq, thr, args.variant)
+        threads = 1
+    rate = cs.size / max(t, 1e-6)
+    stride = max(1, s.size // int(min(s.size, max(2000, rate * 1.5))))
+    ss, sT, sq = strided_sample(s, T, q, stride)
+    opts = O.Options(variant=args.variant, activity_threshold=thr)
+    walls = []
+    for i in range(args.warmup + args.steps):
+        if kind == "reference":
+            w = O.ref_time_run_parallel(ss, sT, sq, opts, n_threads=threads, strategy=2, omp_chunk=1)
+            wall = w["deep"] + w["shallow"]
+        else:
+            wall = cpu_port_time(ss, sT, sq, thr, args.variant)
+        if i >= args.warmup:
+            walls.append(wall)
+    tot = float(np.sum(walls))
+    value = ss.size * len(walls) / tot
+    sample = (f"every {stride}th column of {args.config} ({ss.size} columns) per step; "
+              + ("reference run_parallel Dynamic(omp_chunk=1) deep then shallow" if kind == "reference"
+                 else "serial C oracle"))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(walls),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, gridgen.py)",
+        "config": {"workload": args.config, "n_columns_sample": int(ss.size), "levels": int(T.shape[0]),
+                   "activity_threshold": thr, "variant": args.variant},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_gpu_arm(args):
+    import torch
+    import paper_1711_00289_b200 as P
+    from paper_1711_00289_b200 import gridgen
+
+    ws, rank, local = dist_env()
+    dist = init_dist(ws, "nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    thr = gridgen.config_threshold(args.config)
+    s, T, q = gridgen.make_config(args.config, seed=args.seed)
+    L, n_total = T.shape
+    opts = P.KernelOptions(variant=args.variant, activity_threshold=thr)
+
+    # partition: contiguous ranges balanced by estimated cost
+    hbm_gbs, hbm_src = measured_peaks()
+    deep_w = 159.0 * L + 37.0 * 694.0               # FLOP model, mean U at guess 24+160s
+    shallow_w = 1482.0 * (34.0e12 / (hbm_gbs * 1e9))  # bytes priced at the FP64/HBM ratio
+    if args.partition == "naive":
+        bounds = P.plan_partition(s, thr, ws, 0.0, 1.0)
+    else:
+        bounds = P.plan_partition(s, thr, ws, deep_w, shallow_w)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    n = hi - lo
+    s_r, T_r, q_r = s[lo:hi], np.ascontiguousarray(T[:, lo:hi]), np.ascontiguousarray(q[:, lo:hi])
+
+    ctx = P.Context(local)
+    ds = torch.from_numpy(s_r).to(dev)
+    dT = torch.from_numpy(T_r).to(dev)
+    dq = torch.from_numpy(q_r).to(dev)
+
+    def alloc_out():
+        return (torch.empty((L, n), dtype=torch.float64, device=dev),
+                torch.empty((L, n), dtype=torch.float64, device=dev),
+                torch.empty(n, dtype=torch.float64, device=dev),
+                torch.empty(n, dtype=torch.int64, device=dev),
+                torch.empty(n, dtype=torch.uint8, device=dev))
+
+    deep_o, sh_o = alloc_out(), alloc_out()
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        ctx.convect_async(ds, dT, dq, deep_o, sh_o, opts, P.BOTH, first_col=lo, stream=stream)
+
+    # warm-up (W >= 3 enforced) and error check
+    W = max(3, args.warmup)
+    for _ in range(W):
+        step()
+    st = ctx.check(stream)
+    n_trig_local = st.n_triggered
+
+    # timed region: K steps, barrier + sync on both sides, device events on the launching stream
+    K = args.steps
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ctx.profile_begin(K)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(K):
+            step()
+        ev1.record(stream)
+        stream.synchronize()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    kern = ctx.profile_end(K)  # [K][3] trigger, deep, shallow (ms)
+    ctx.check(stream)
+
+    # max over ranks
+    t = torch.tensor([ms_local, n_trig_local, n], dtype=torch.float64, device=dev)
+    if dist:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+        ms_total, n_trig = float(tmax[0]), int(tsum[1])
+    else:
+        ms_total, n_trig = ms_local, n_trig_local
+    ms_step = ms_total / K
+    value = n_total * K / (ms_total * 1e-3)
+
+    # model FLOPs from this rank's outputs (work_units / exit flags match the oracle)
+    dw = deep_o[3].cpu().numpy()
+    dx = deep_o[4].cpu().numpy()
+    sw = sh_o[3].cpu().numpy()
+    sx = sh_o[4].cpu().numpy()
+    deep_flops, sh_flops, trig_r = flop_model(L, dw, dx, sw, sx)
+
+    # FP64 peak measured live on this device
+    fp64_peak = ctx.fp64_peak_tflops(5)
+    deep_ms = float(np.mean(kern[:, 1])) if len(kern) else float("nan")
+    trig_ms = float(np.mean(kern[:, 0])) if len(kern) else float("nan")
+    sh_ms = float(np.mean(kern[:, 2])) if len(kern) else float("nan")
+    achieved = deep_flops / (deep_ms * 1e-3) / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "deep_traffic.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                d = json.load(f)
+            if d.get("config") == args.config and ws == 1:
+                traffic = d.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    bytes_step, per_col, deep_bytes = bytes_model(n, L, trig_r)
+    t_flop = (deep_flops + sh_flops) / (fp64_peak * 1e12)
+    t_hbm = bytes_step / (hbm_gbs * 1e9)
+    t_roof = max(t_flop, t_hbm)
+
+    # ---- end-to-end through the public host API (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        pin = [P.PinnedArray(a.shape, a.dtype) for a in (s_r, T_r, q_r)]
+        for pa, a in zip(pin, (s_r, T_r, q_r)):
+            pa.array[...] = a
+
+        def pinned_out():
+            arrs = [P.PinnedArray((L, n)), P.PinnedArray((L, n)), P.PinnedArray((n,)),
+                    P.PinnedArray((n,), np.int64), P.PinnedArray((n,), np.uint8)]
+            return arrs, P.ColumnOutputs(*[a.array for a in arrs])
+
+        pdo, out_d = pinned_out()
+        pso, out_s = pinned_out()
+        for _ in range(2):
+            ctx.convect(pin[0].array, pin[1].array, pin[2].array, opts, P.BOTH, lo, out_d, out_s)
+        Ke = max(1, min(K, args.e2e_steps))
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(Ke):
+            ctx.convect(pin[0].array, pin[1].array, pin[2].array, opts, P.BOTH, lo, out_d, out_s)
+        el = time.perf_counter() - t0
+        stt = ctx.last_stats
+        te = torch.tensor([el], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te[0])
+        e2e = {"value": n_total * Ke / el, "unit": UNIT, "h2d_bytes_per_step": int(stt.h2d_bytes),
+               "d2h_bytes_per_step": int(stt.d2h_bytes), "steps": Ke,
+               "ms_per_step": 1e3 * el / Ke,
+               "note": "cvg_convect (C ABI) on pinned host SoA buffers: H2D inputs, compute, D2H all outputs, per step; wall clock, max over ranks"}
+        for a in pin + pdo + pso:
+            a.free()
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(s, T, q, thr, args.variant)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator, paper_1711_00289_b200/gridgen.py)",
+        "config": {"workload": args.config, "n_columns": int(n_total), "levels": int(L),
+                   "activity_threshold": thr, "variant": args.variant,
+                   "triggered_deep": int(n_trig), "partition": args.partition if ws > 1 else "single",
+                   "l2": "inputs (425 MB) + outputs (880 MB) exceed the 126 MB L2; no flush needed",
+                   "parallelism": f"column partition x{ws}, no collective"},
+        "roofline": {"bound": "fp64", "kernel": "deep_kernel", "achieved": achieved,
+                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                     "traffic": traffic,
+                     "peak_source": "live DFMA probe on this GPU (cvg_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
+                     "flops_per_launch": deep_flops, "ms_per_launch": deep_ms,
+                     "model": "159*L + 37*U_c FLOP per triggered column (SURVEY 8d), U_c from the step's work_units"},
+        "step_roofline": {"flops": deep_flops + sh_flops, "bytes": bytes_step, "bytes_per_column": per_col,
+                          "t_fp64_ms": 1e3 * t_flop, "t_hbm_ms": 1e3 * t_hbm,
+                          "hbm_peak_gbs": hbm_gbs, "hbm_source": hbm_src,
+                          "fp64_peak_tflops": fp64_peak,
+                          "bound": "fp64" if t_flop >= t_hbm else "hbm",
+                          "roofline_ms": 1e3 * t_roof, "frac": 1e3 * t_roof / (ms_total / K) if ws == 1 else None},
+        "kernels_ms": {"trigger_compact": trig_ms, "deep": deep_ms, "shallow_zero": sh_ms},
+        "gpu_launches": 3 * K,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=["ref", "c1", "c2", "c3", "c4", "c5_05", "c5_50", "c5_95"])
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--partition", default="balanced", choices=["balanced", "naive"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

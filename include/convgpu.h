@@ -171,6 +171,25 @@ cvg_status cvg_plan_partition(long long n, const double* s,
                               double deep_weight, double shallow_weight,
                               long long* bounds);
 
+/* --- Measurement support (bench.py) ----------------------------------- */
+
+/* Per-kernel device timing: while enabled, every cvg_convect_async call
+ * records CUDA events around each of its kernels on the launching stream
+ * (slots for up to max_steps calls).  cvg_profile_end returns, per recorded
+ * call, the durations in ms of [trigger+compaction, deep, shallow] (row-major
+ * [n_steps][3], 0 for a kernel not launched) and disables recording. */
+cvg_status cvg_profile_begin(cvg_context* ctx, int max_steps);
+cvg_status cvg_profile_end(cvg_context* ctx, int* n_steps, double* kernel_ms, int capacity);
+
+/* FP64 pipe peak of this device, measured now: a DFMA-chain probe over all
+ * SMs (2 FLOP per DFMA), best of `reps` launches.  This is the FP64
+ * roofline denominator (MEASURED_PEAKS.json carries no FP64 figure). */
+cvg_status cvg_fp64_peak(cvg_context* ctx, int reps, double* tflops);
+
+/* Page-locked host memory for staging (cudaMallocHost). */
+cvg_status cvg_host_alloc(size_t bytes, void** out);
+void cvg_host_free(void* p);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -125,7 +125,14 @@ def load_library():
     L.cvg_ientropy_solve.argtypes = [vp, i64, vp, vp, C.POINTER(KernelOptions), vp, vp]
     L.cvg_approx_exp.argtypes = [vp, i64, vp, vp]
     L.cvg_plan_partition.argtypes = [i64, vp, dbl, i32, dbl, dbl, vp]
-    for f in ("cvg_context_create", "cvg_convect", "cvg_convect_async", "cvg_convect_check",
+    L.cvg_profile_begin.argtypes = [vp, i32]
+    L.cvg_profile_end.argtypes = [vp, C.POINTER(C.c_int), vp, i32]
+    L.cvg_fp64_peak.argtypes = [vp, i32, C.POINTER(C.c_double)]
+    L.cvg_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
+    L.cvg_host_free.argtypes = [vp]
+    L.cvg_host_free.restype = None
+    for f in ("cvg_profile_begin", "cvg_profile_end", "cvg_fp64_peak", "cvg_host_alloc",
+              "cvg_context_create", "cvg_convect", "cvg_convect_async", "cvg_convect_check",
               "cvg_deep_convection", "cvg_shallow_convection", "cvg_ientropy_solve",
               "cvg_approx_exp", "cvg_plan_partition"):
         getattr(L, f).restype = C.c_int
@@ -206,14 +213,16 @@ class Context:
         self.close()
 
     # -- host (numpy) entry points -------------------------------------------
-    def convect(self, s, T, q, opts: KernelOptions | None = None, kernels=BOTH, first_col=0):
+    def convect(self, s, T, q, opts: KernelOptions | None = None, kernels=BOTH, first_col=0,
+                out_deep: ColumnOutputs | None = None, out_shallow: ColumnOutputs | None = None):
         """Runs deep and/or shallow over host SoA arrays; returns (deep, shallow)
-        ColumnOutputs (None for a kernel not requested)."""
+        ColumnOutputs (None for a kernel not requested).  Preallocated (e.g.
+        pinned) output buffers may be passed in."""
         opts = opts or KernelOptions()
         keep, cols = _host_columns(s, T, q, first_col)
         L, n = keep[1].shape
-        deep = ColumnOutputs.empty(n, L) if kernels & DEEP else None
-        sh = ColumnOutputs.empty(n, L) if kernels & SHALLOW else None
+        deep = (out_deep or ColumnOutputs.empty(n, L)) if kernels & DEEP else None
+        sh = (out_shallow or ColumnOutputs.empty(n, L)) if kernels & SHALLOW else None
         st = Stats()
         rc = load_library().cvg_convect(self._h, C.byref(cols), C.byref(opts), kernels,
                                         C.byref(deep._struct()) if deep else None,
@@ -270,6 +279,21 @@ class Context:
                                               outs(deep), outs(shallow), h)
         _raise(rc)
 
+    def profile_begin(self, max_steps: int):
+        _raise(load_library().cvg_profile_begin(self._h, int(max_steps)))
+
+    def profile_end(self, capacity: int = 4096) -> np.ndarray:
+        """[n_steps][3] kernel durations (ms): trigger+compaction, deep, shallow."""
+        buf = np.zeros((capacity, 3))
+        n = C.c_int()
+        _raise(load_library().cvg_profile_end(self._h, C.byref(n), buf.ctypes.data, capacity))
+        return buf[: n.value].copy()
+
+    def fp64_peak_tflops(self, reps: int = 5) -> float:
+        v = C.c_double()
+        _raise(load_library().cvg_fp64_peak(self._h, int(reps), C.byref(v)))
+        return v.value
+
     def check(self, stream=None) -> Stats:
         st = Stats()
         h = None if stream is None else getattr(stream, "cuda_stream", stream)
@@ -277,6 +301,25 @@ class Context:
         self.last_stats = st
         _raise(rc, st)
         return st
+
+
+class PinnedArray:
+    """Page-locked host buffer (cvg_host_alloc) viewed as a numpy array."""
+
+    def __init__(self, shape, dtype=np.float64):
+        dt = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dt.itemsize
+        p = C.c_void_p()
+        _raise(load_library().cvg_host_alloc(nbytes, C.byref(p)))
+        self._p = p
+        buf = (C.c_char * max(nbytes, 1)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+    def free(self):
+        if self._p:
+            self.array = None
+            load_library().cvg_host_free(self._p)
+            self._p = None
 
 
 _default_ctx: Context | None = None

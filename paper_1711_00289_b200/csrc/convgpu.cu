@@ -118,6 +118,11 @@ struct cvg_context {
   DevBuf<uint8_t> dx, sx;
   DevBuf<double> aux0, aux1;
   DevBuf<int> auxi;
+  // per-kernel profiling (cvg_profile_begin/end)
+  bool prof_on = false;
+  int prof_cap = 0, prof_n = 0;
+  std::vector<cudaEvent_t> prof_ev;  // 4 per step: start, after trigger, after deep, after shallow
+  int prof_mask_first = 0;
   // last async call
   int last_mask = 0;
   int last_maxit = 100;
@@ -180,6 +185,9 @@ void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int 
   CVG_CUDA(cudaMemsetAsync(ctx->err.p, 0xff, 2 * sizeof(unsigned long long), st));
   if (n == 0) return;
   const bool do_deep = (mask & CVG_DEEP) != 0, do_sh = (mask & CVG_SHALLOW) != 0;
+  cudaEvent_t* pe = nullptr;
+  if (ctx->prof_on && ctx->prof_n < ctx->prof_cap) pe = &ctx->prof_ev[4 * ctx->prof_n++];
+  if (pe) CVG_CUDA(cudaEventRecord(pe[0], st));
   if (do_deep) {
     ctx->idx.ensure((size_t)n);
     const unsigned tb = (unsigned)((n + cvg::kTrigTile - 1) / cvg::kTrigTile);
@@ -195,12 +203,16 @@ void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int 
     a.thr = o->activity_threshold; a.tol = o->newton_tol; a.maxit = o->newton_max_iter;
     a.L = L; a.cpb = pick_cpb(L);
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
+    if (pe) CVG_CUDA(cudaEventRecord(pe[1], st));
     switch (o->variant) {
       case 1: launch_deep<cvg::kVarReduced>(ctx, a, st); break;
       case 2: launch_deep<cvg::kVarApprox>(ctx, a, st); break;
       default: launch_deep<cvg::kVarExact>(ctx, a, st); break;
     }
+  } else if (pe) {
+    CVG_CUDA(cudaEventRecord(pe[1], st));
   }
+  if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
   if (do_sh || do_deep) {
     cvg::ShallowArgs b{};
     b.s = in->s; b.T = in->T; b.q = in->q; b.ld_in = in->ld; b.n = n;
@@ -220,6 +232,7 @@ void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int 
       default: launch_shallow<cvg::kVarExact>(b, do_sh, do_deep, st); break;
     }
   }
+  if (pe) CVG_CUDA(cudaEventRecord(pe[3], st));
 }
 
 // Reads back the latched failure words (stream already synchronised).
@@ -370,6 +383,7 @@ void cvg_context_free(cvg_context* ctx) {
   if (ctx->h_count) cudaFreeHost(ctx->h_count);
   for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->ev_h0, ctx->ev_h1, ctx->ev_d0})
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -558,6 +572,82 @@ cvg_status cvg_approx_exp(cvg_context* ctx, long long n, const double* x, double
     CVG_CUDA(cudaStreamSynchronize(st));
     return CVG_OK;
   });
+}
+
+cvg_status cvg_profile_begin(cvg_context* ctx, int max_steps) {
+  if (!ctx || max_steps < 1) return fail(CVG_ERR_INVALID, "cvg_profile_begin: null context or max_steps < 1");
+  return guarded([&] {
+    CVG_CUDA(cudaSetDevice(ctx->device));
+    const size_t need = 4 * (size_t)max_steps;
+    while (ctx->prof_ev.size() < need) {
+      cudaEvent_t e;
+      CVG_CUDA(cudaEventCreate(&e));
+      ctx->prof_ev.push_back(e);
+    }
+    ctx->prof_cap = max_steps;
+    ctx->prof_n = 0;
+    ctx->prof_on = true;
+    return CVG_OK;
+  });
+}
+
+cvg_status cvg_profile_end(cvg_context* ctx, int* n_steps, double* kernel_ms, int capacity) {
+  if (!ctx || !n_steps) return fail(CVG_ERR_INVALID, "cvg_profile_end: null argument");
+  return guarded([&] {
+    CVG_CUDA(cudaSetDevice(ctx->device));
+    ctx->prof_on = false;
+    const int n = std::min(ctx->prof_n, capacity);
+    for (int i = 0; i < n; ++i) {
+      cudaEvent_t* pe = &ctx->prof_ev[4 * i];
+      CVG_CUDA(cudaEventSynchronize(pe[3]));
+      for (int k = 0; k < 3; ++k) {
+        float ms = 0.f;
+        CVG_CUDA(cudaEventElapsedTime(&ms, pe[k], pe[k + 1]));
+        if (kernel_ms) kernel_ms[3 * i + k] = ms;
+      }
+    }
+    *n_steps = n;
+    ctx->prof_n = 0;
+    return CVG_OK;
+  });
+}
+
+cvg_status cvg_fp64_peak(cvg_context* ctx, int reps, double* tflops) {
+  if (!ctx || !tflops) return fail(CVG_ERR_INVALID, "cvg_fp64_peak: null argument");
+  return guarded([&] {
+    CVG_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int blocks = ctx->num_sms * 8, threads = 256, iters = 4096;
+    ctx->aux0.ensure((size_t)blocks * threads);
+    for (int w = 0; w < 2; ++w)
+      cvg::dfma_probe_kernel<<<blocks, threads, 0, st>>>(ctx->aux0.p, iters, 0.999999, 1e-7);
+    CVG_CUDA(cudaGetLastError());
+    float best = 1e30f;
+    for (int r = 0; r < std::max(reps, 1); ++r) {
+      CVG_CUDA(cudaEventRecord(ctx->ev0, st));
+      cvg::dfma_probe_kernel<<<blocks, threads, 0, st>>>(ctx->aux0.p, iters, 0.999999, 1e-7);
+      CVG_CUDA(cudaEventRecord(ctx->ev1, st));
+      CVG_CUDA(cudaEventSynchronize(ctx->ev1));
+      float ms = 0.f;
+      CVG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+      best = std::min(best, ms);
+    }
+    const double flops = 2.0 * 8.0 * (double)blocks * threads * iters;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return CVG_OK;
+  });
+}
+
+cvg_status cvg_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(CVG_ERR_INVALID, "cvg_host_alloc: null out");
+  return guarded([&] {
+    CVG_CUDA(cudaMallocHost(out, std::max<size_t>(bytes, 1)));
+    return CVG_OK;
+  });
+}
+
+void cvg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 cvg_status cvg_plan_partition(long long n, const double* s, double thr, int n_parts, double deep_weight,

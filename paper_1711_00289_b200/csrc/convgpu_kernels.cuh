@@ -417,6 +417,21 @@ __global__ void ientropy_kernel(const double* __restrict__ y, const double* __re
   raise_failure(err, i, 0, kFailNoConv);
 }
 
+// FP64 roofline probe: 8 independent DFMA chains per thread.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) x[c] = threadIdx.x * 1e-3 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = fma(x[c], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += x[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void approx_exp_kernel(const double* __restrict__ x, double* __restrict__ o, long long n) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) o[i] = approx_exp_ref(x[i]);
