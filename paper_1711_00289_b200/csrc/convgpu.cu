@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -90,25 +91,20 @@ const char* kind_message(int kind, int kernel, int maxit, std::string* buf) {
   }
 }
 
-int pick_cpb(int L) {
-  const int hi = std::max(1, 512 / L);
-  for (int c = hi; c >= std::max(1, hi / 2); --c) {
-    if ((c * L) % 32 == 0) return c;
-  }
-  return hi;
-}
-
 }  // namespace
 
 struct cvg_context {
   int device = 0;
   int num_sms = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;           // shallow kernel, concurrent with deep
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_h0 = nullptr, ev_h1 = nullptr, ev_d0 = nullptr;
   DevBuf<double2> exp_tab;
   DevBuf<int> idx;
-  DevBuf<int> counters;                // [0] triggered count, [1] deep tile cursor
+  DevBuf<int> counters;                // [0] triggered count, [2..3] deep work cursor (u64)
   DevBuf<unsigned long long> err;      // [0] deep, [1] shallow, [2] ientropy
+  DevBuf<unsigned long long> cursor;   // deep work cursor + 32 dummy words
   unsigned long long* h_err = nullptr; // pinned mirror
   int* h_count = nullptr;
   // staging for host-buffer calls
@@ -118,10 +114,13 @@ struct cvg_context {
   DevBuf<uint8_t> dx, sx;
   DevBuf<double> aux0, aux1;
   DevBuf<int> auxi;
+  int col_warps = 8;                   // column-stream warps per fused block
+  bool fused = false;                  // fused persistent kernel vs split kernels
+  int shallow_mode = 0;                // 0 plain, 1 L2-prefetched stream, 2 TMA-staged
   // per-kernel profiling (cvg_profile_begin/end)
   bool prof_on = false;
   int prof_cap = 0, prof_n = 0;
-  std::vector<cudaEvent_t> prof_ev;  // 4 per step: start, after trigger, after deep, after shallow
+  std::vector<cudaEvent_t> prof_ev;  // 5 per step: start, after trigger, after deep (main stream), shallow start/end (side)
   int prof_mask_first = 0;
   // last async call
   int last_mask = 0;
@@ -155,81 +154,139 @@ bool valid_options(const cvg_options* o, std::string* why) {
   return true;
 }
 
-template <int VAR>
-void launch_deep(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
-  const int threads = ((a.cpb * a.L + 31) / 32) * 32;
-  const size_t smem = cvg::kExpTableSize * sizeof(double2) + (size_t)a.cpb * a.L * (sizeof(double) + sizeof(int)) +
-                      (size_t)a.cpb * sizeof(int);
-  int occ = 0;
-  CVG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cvg::deep_kernel<VAR>, threads, smem));
-  occ = std::max(occ, 1);
-  cvg::deep_kernel<VAR><<<ctx->num_sms * occ, threads, smem, st>>>(a);
+// Launch of the fused persistent kernel (cvg::convect_kernel): one block per
+// SM; n_col_warps of its warps stream the shallow scheme + deep zero-fill
+// while the rest work the compacted deep list.
+template <int VAR, bool NARROW, bool SH, bool DP>
+void launch_fused_t(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, int n_col_warps,
+                    cudaStream_t st) {
+  const int threads = cvg::kFusedWarps * 32;
+  const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
+                      (DP ? (size_t)cvg::kFusedWarps * a.batch * a.L * sizeof(double) : 0);
+  auto kern = cvg::convect_kernel<VAR, NARROW, SH, DP>;
+  CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<ctx->num_sms, threads, smem, st>>>(a, b, n_col_warps, ctx->cursor.p + 40);
+  CVG_CUDA(cudaGetLastError());
+}
+
+template <int VAR, bool NARROW>
+void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
+  const int threads = cvg::kFusedWarps * 32;
+  const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
+                      (size_t)cvg::kFusedWarps * a.batch * a.L * sizeof(double);
+  auto kern = cvg::deep_kernel<VAR, NARROW>;
+  CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<ctx->num_sms, threads, smem, st>>>(a);
   CVG_CUDA(cudaGetLastError());
 }
 
 template <int VAR>
-void launch_shallow(const cvg::ShallowArgs& a, bool do_sh, bool do_zero, cudaStream_t st) {
-  const unsigned blocks = (unsigned)((a.n + 255) / 256);
-  if (do_sh && do_zero) cvg::shallow_kernel<VAR, true, true><<<blocks, 256, 0, st>>>(a);
-  else if (do_sh) cvg::shallow_kernel<VAR, true, false><<<blocks, 256, 0, st>>>(a);
-  else if (do_zero) cvg::shallow_kernel<VAR, false, true><<<blocks, 256, 0, st>>>(a);
+void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh, bool dp,
+                  cudaEvent_t* pe, cudaStream_t st) {
+  if (dp) {
+    if (a.L <= 32) launch_deep_t<VAR, true>(ctx, a, st);
+    else launch_deep_t<VAR, false>(ctx, a, st);
+  }
+  if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
+  if (ctx->shallow_mode == 1) {
+    int occ = 0;
+    auto k = sh && dp ? cvg::shallow_stream_kernel<VAR, true, true>
+                      : sh ? cvg::shallow_stream_kernel<VAR, true, false>
+                           : cvg::shallow_stream_kernel<VAR, false, true>;
+    CVG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, 0));
+    k<<<ctx->num_sms * std::max(occ, 1), 128, 0, st>>>(b);
+  } else if (ctx->shallow_mode == 2 && (b.ld_in % 2) == 0) {
+    const size_t smem = (size_t)cvg::kExpTableSize * sizeof(double2) +
+                        (size_t)2 * 2 * b.L * cvg::kShTile * sizeof(double);
+    auto k = sh && dp ? cvg::shallow_tma_kernel<VAR, true, true>
+                      : sh ? cvg::shallow_tma_kernel<VAR, true, false> : cvg::shallow_tma_kernel<VAR, false, true>;
+    CVG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<ctx->num_sms, cvg::kShTile, smem, st>>>(b);
+  } else {
+    const unsigned blocks = (unsigned)((b.n + cvg::kShallowThreads - 1) / cvg::kShallowThreads);
+    if (sh && dp) cvg::shallow_kernel<VAR, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    else if (sh) cvg::shallow_kernel<VAR, true, false><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    else if (dp) cvg::shallow_kernel<VAR, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+  }
   CVG_CUDA(cudaGetLastError());
 }
 
-// Enqueues the hot path on `st`.  Pointers are device pointers.
+template <int VAR>
+void launch_fused(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh, bool dp,
+                  int n_col_warps, cudaStream_t st) {
+  const bool narrow = a.L <= 32;
+  if (sh && dp) {
+    if (narrow) launch_fused_t<VAR, true, true, true>(ctx, a, b, n_col_warps, st);
+    else launch_fused_t<VAR, false, true, true>(ctx, a, b, n_col_warps, st);
+  } else if (dp) {
+    if (narrow) launch_fused_t<VAR, true, false, true>(ctx, a, b, n_col_warps, st);
+    else launch_fused_t<VAR, false, false, true>(ctx, a, b, n_col_warps, st);
+  } else {
+    launch_fused_t<VAR, true, true, false>(ctx, a, b, cvg::kFusedWarps, st);
+  }
+}
+
+// Enqueues the hot path on `st`: memsets of the per-call cursors and
+// failure words, the trigger + compaction kernel (deep requested), then the
+// fused persistent kernel.  Pointers are device pointers.
 void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int mask,
              const cvg_outputs* deep, const cvg_outputs* sh, cudaStream_t st) {
   const long long n = in->n_columns;
   const int L = in->n_levels;
-  CVG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 2 * sizeof(int), st));
+  CVG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(int), st));
+  CVG_CUDA(cudaMemsetAsync(ctx->cursor.p, 0, sizeof(unsigned long long), st));
+  CVG_CUDA(cudaMemsetAsync(ctx->cursor.p + 40, 0, sizeof(unsigned long long), st));
   CVG_CUDA(cudaMemsetAsync(ctx->err.p, 0xff, 2 * sizeof(unsigned long long), st));
   if (n == 0) return;
   const bool do_deep = (mask & CVG_DEEP) != 0, do_sh = (mask & CVG_SHALLOW) != 0;
   cudaEvent_t* pe = nullptr;
   if (ctx->prof_on && ctx->prof_n < ctx->prof_cap) pe = &ctx->prof_ev[4 * ctx->prof_n++];
   if (pe) CVG_CUDA(cudaEventRecord(pe[0], st));
+  cvg::DeepArgs a{};
   if (do_deep) {
     ctx->idx.ensure((size_t)n);
     const unsigned tb = (unsigned)((n + cvg::kTrigTile - 1) / cvg::kTrigTile);
     cvg::trigger_compact_kernel<<<tb, cvg::kTrigThreads, 0, st>>>(
         in->s, n, o->activity_threshold, ctx->idx.p, ctx->counters.p, ctx->err.p);
     CVG_CUDA(cudaGetLastError());
-    cvg::DeepArgs a{};
     a.s = in->s; a.T = in->T; a.q = in->q; a.ld_in = in->ld;
     a.tend_T = deep->tend_T; a.tend_q = deep->tend_q; a.precip = deep->precip;
     a.work = deep->work_units; a.exited = deep->exited_early; a.ld_out = deep->ld;
-    a.idx = ctx->idx.p; a.count = ctx->counters.p; a.tile_cursor = ctx->counters.p + 1;
-    a.err = ctx->err.p; a.exp_tab = ctx->exp_tab.p; a.first_col = in->first_col;
+    a.idx = ctx->idx.p; a.count = ctx->counters.p;
+    a.cursor = ctx->cursor.p;
+    a.err = ctx->err.p; a.first_col = in->first_col;
     a.thr = o->activity_threshold; a.tol = o->newton_tol; a.maxit = o->newton_max_iter;
-    a.L = L; a.cpb = pick_cpb(L);
+    a.L = L;
+    a.batch = std::max(1, std::min(cvg::kDeepBatch, (int)(98304 / ((size_t)cvg::kFusedWarps * L * sizeof(double)))));
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
-    if (pe) CVG_CUDA(cudaEventRecord(pe[1], st));
-    switch (o->variant) {
-      case 1: launch_deep<cvg::kVarReduced>(ctx, a, st); break;
-      case 2: launch_deep<cvg::kVarApprox>(ctx, a, st); break;
-      default: launch_deep<cvg::kVarExact>(ctx, a, st); break;
-    }
-  } else if (pe) {
-    CVG_CUDA(cudaEventRecord(pe[1], st));
   }
-  if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
-  if (do_sh || do_deep) {
-    cvg::ShallowArgs b{};
-    b.s = in->s; b.T = in->T; b.q = in->q; b.ld_in = in->ld; b.n = n;
-    if (do_sh) {
-      b.tend_T = sh->tend_T; b.tend_q = sh->tend_q; b.precip = sh->precip;
-      b.work = sh->work_units; b.exited = sh->exited_early; b.ld_out = sh->ld;
-    }
-    if (do_deep) {
-      b.d_tend_T = deep->tend_T; b.d_tend_q = deep->tend_q; b.d_precip = deep->precip;
-      b.d_work = deep->work_units; b.d_exited = deep->exited_early; b.d_ld_out = deep->ld;
-    }
-    b.err = ctx->err.p + 1; b.exp_tab = ctx->exp_tab.p; b.first_col = in->first_col;
-    b.thr = o->activity_threshold; b.L = L;
+  a.exp_tab = ctx->exp_tab.p;
+  if (pe) CVG_CUDA(cudaEventRecord(pe[1], st));
+  cvg::ShallowArgs b{};
+  b.s = in->s; b.T = in->T; b.q = in->q; b.ld_in = in->ld; b.n = n;
+  if (do_sh) {
+    b.tend_T = sh->tend_T; b.tend_q = sh->tend_q; b.precip = sh->precip;
+    b.work = sh->work_units; b.exited = sh->exited_early; b.ld_out = sh->ld;
+  }
+  if (do_deep) {
+    b.d_tend_T = deep->tend_T; b.d_tend_q = deep->tend_q; b.d_precip = deep->precip;
+    b.d_work = deep->work_units; b.d_exited = deep->exited_early; b.d_ld_out = deep->ld;
+  }
+  b.err = ctx->err.p + 1; b.exp_tab = ctx->exp_tab.p; b.first_col = in->first_col;
+  b.thr = o->activity_threshold; b.L = L;
+  const int ncw = std::min(cvg::kFusedWarps, std::max(1, ctx->col_warps));
+  if (ctx->fused) {
     switch (o->variant) {
-      case 1: launch_shallow<cvg::kVarReduced>(b, do_sh, do_deep, st); break;
-      case 2: launch_shallow<cvg::kVarApprox>(b, do_sh, do_deep, st); break;
-      default: launch_shallow<cvg::kVarExact>(b, do_sh, do_deep, st); break;
+      case 1: launch_fused<cvg::kVarReduced>(ctx, a, b, do_sh, do_deep, ncw, st); break;
+      case 2: launch_fused<cvg::kVarApprox>(ctx, a, b, do_sh, do_deep, ncw, st); break;
+      default: launch_fused<cvg::kVarExact>(ctx, a, b, do_sh, do_deep, ncw, st); break;
+    }
+    if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
+  } else {
+    switch (o->variant) {
+      case 1: launch_split<cvg::kVarReduced>(ctx, a, b, do_sh, do_deep, pe, st); break;
+      case 2: launch_split<cvg::kVarApprox>(ctx, a, b, do_sh, do_deep, pe, st); break;
+      default: launch_split<cvg::kVarExact>(ctx, a, b, do_sh, do_deep, pe, st); break;
     }
   }
   if (pe) CVG_CUDA(cudaEventRecord(pe[3], st));
@@ -337,6 +394,9 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     ctx->num_sms = prop.multiProcessorCount;
     try {
       CVG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      CVG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+      CVG_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+      CVG_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
       CVG_CUDA(cudaEventCreate(&ctx->ev0));
       CVG_CUDA(cudaEventCreate(&ctx->ev1));
       CVG_CUDA(cudaEventCreate(&ctx->ev_h0));
@@ -346,14 +406,17 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
       ctx->exp_tab.ensure(tab.size());
       CVG_CUDA(cudaMemcpy(ctx->exp_tab.p, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
       ctx->counters.ensure(4);
+      ctx->cursor.ensure(80);  // [0] deep cursor, [40] tile cursor, others dummies
+      CVG_CUDA(cudaMemset(ctx->cursor.p, 0, 80 * sizeof(unsigned long long)));
       ctx->err.ensure(4);
       CVG_CUDA(cudaMallocHost(&ctx->h_err, 4 * sizeof(unsigned long long)));
       CVG_CUDA(cudaMallocHost(&ctx->h_count, 4 * sizeof(int)));
       CVG_CUDA(cudaMemset(ctx->counters.p, 0, 4 * sizeof(int)));
       CVG_CUDA(cudaMemset(ctx->err.p, 0xff, 4 * sizeof(unsigned long long)));
       // probe that the sm_100a image loads on this device
-      CVG_CUDA(cudaFuncSetAttribute(cvg::deep_kernel<cvg::kVarExact>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, 50));
+      if (const char* e = getenv("CVG_COL_WARPS")) ctx->col_warps = atoi(e);
+      if (const char* e = getenv("CVG_FUSED")) ctx->fused = atoi(e) != 0;
+      if (const char* e = getenv("CVG_SHALLOW_MODE")) ctx->shallow_mode = atoi(e);
     } catch (...) {
       cvg_context_free(ctx);
       throw;
@@ -370,6 +433,7 @@ void cvg_context_free(cvg_context* ctx) {
   for (auto* b : {&ctx->exp_tab}) b->release();
   ctx->idx.release();
   ctx->counters.release();
+  ctx->cursor.release();
   ctx->err.release();
   for (auto* b : {&ctx->in_s, &ctx->in_T, &ctx->in_q, &ctx->dT, &ctx->dq, &ctx->dp, &ctx->sT, &ctx->sq, &ctx->sp,
                   &ctx->aux0, &ctx->aux1})
@@ -385,6 +449,9 @@ void cvg_context_free(cvg_context* ctx) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 
@@ -600,10 +667,14 @@ cvg_status cvg_profile_end(cvg_context* ctx, int* n_steps, double* kernel_ms, in
     for (int i = 0; i < n; ++i) {
       cudaEvent_t* pe = &ctx->prof_ev[4 * i];
       CVG_CUDA(cudaEventSynchronize(pe[3]));
-      for (int k = 0; k < 3; ++k) {
-        float ms = 0.f;
-        CVG_CUDA(cudaEventElapsedTime(&ms, pe[k], pe[k + 1]));
-        if (kernel_ms) kernel_ms[3 * i + k] = ms;
+      float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+      CVG_CUDA(cudaEventElapsedTime(&t0, pe[0], pe[1]));
+      CVG_CUDA(cudaEventElapsedTime(&t1, pe[1], pe[2]));
+      CVG_CUDA(cudaEventElapsedTime(&t2, pe[2], pe[3]));
+      if (kernel_ms) {
+        kernel_ms[3 * i + 0] = t0;
+        kernel_ms[3 * i + 1] = t1;
+        kernel_ms[3 * i + 2] = t2;
       }
     }
     *n_steps = n;

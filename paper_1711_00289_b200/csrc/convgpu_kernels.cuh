@@ -5,11 +5,12 @@
 //                           dense list of triggered columns (replaces the
 //                           reference's dynamic scheduling, sched.cpp:166-173)
 //   deep_kernel             deep plume (physics.cpp:106-166) over the
-//                           compacted list: one lane per (column, level), each
-//                           lane runs its level's entrainment then
-//                           precipitation Newton solve (physics.cpp:64-87);
-//                           persistent blocks pull tiles of columns from an
-//                           atomic cursor; ordered precip sum per column
+//                           compacted list: one warp per column, one lane per
+//                           level, each lane running its level's entrainment
+//                           and precipitation Newton solves (physics.cpp:
+//                           64-87) in lockstep; persistent warps walk the list
+//                           cyclically with the next column prefetched;
+//                           ordered precip sum per column inside the warp
 //   shallow_kernel          shallow scheme (physics.cpp:168-225), one thread
 //                           per column, streaming level-major rows, fused with
 //                           the zero-fill of untriggered deep columns
@@ -24,6 +25,7 @@
 #pragma once
 #include <cstdint>
 
+#include "bulkcopy.cuh"
 #include "colmath.cuh"
 
 namespace cvg {
@@ -35,67 +37,90 @@ enum : int { kFailNone = 0, kFailActivity = 1, kFailInput = 2, kFailDiverged = 3
 // reference would have met (entrainment k, then precipitation k), then kind.
 __device__ __forceinline__ void raise_failure(unsigned long long* err, long long col, int order,
                                               int kind) {
-  atomicMin(err, ((unsigned long long)col << 16) | ((unsigned long long)order << 3) |
-                     (unsigned long long)kind);
+  const unsigned long long key =
+      ((unsigned long long)col << 16) | ((unsigned long long)order << 3) | (unsigned long long)kind;
+  asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(err), "l"(key) : "memory");
 }
 
 __device__ __forceinline__ double max0(double x) { return (0.0 < x) ? x : 0.0; }
 
 // ---------------------------------------------------------------------------
 // Trigger + stream compaction.  Each 1024-thread block owns a tile of 4096
-// consecutive columns (4 per thread, coalesced); triggered columns of a tile
-// are written contiguously and in column order (warp ballot + block scan),
-// and one atomicAdd per block reserves the tile's slice of the list.
+// consecutive columns (4 per thread, coalesced).  A triggered column's Newton
+// work is set almost entirely by its guess 24 + 160 s (physics.cpp:121;
+// iteration count is monotone in the guess, physics.hpp:103-107), so the
+// tile's triggered columns are written bucketed by s (kTrigBuckets buckets
+// over (thr, 1]), column order inside a bucket: warps of the deep kernel then
+// hold columns of near-equal work.  __match_any_sync ranks lanes within a
+// (bucket, warp) group, a block scan over (bucket, slot, warp) counts gives
+// the offsets, and one atomicAdd per block reserves the tile's slice.
 constexpr int kTrigThreads = 1024;
 constexpr int kTrigPerThread = 4;
 constexpr int kTrigTile = kTrigThreads * kTrigPerThread;
+constexpr int kTrigBuckets = 16;
 
 __global__ void __launch_bounds__(kTrigThreads)
 trigger_compact_kernel(const double* __restrict__ s, long long n, double thr,
                        int* __restrict__ idx, int* __restrict__ count,
                        unsigned long long* __restrict__ err_deep) {
-  __shared__ int s_cnt[kTrigPerThread * 32];
+  constexpr int kSlots = kTrigBuckets * kTrigPerThread * 32;  // (bucket, i, warp)
+  __shared__ int s_cnt[kSlots];
+  __shared__ int s_wsum[32];
   __shared__ int s_base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long tile0 = (long long)blockIdx.x * kTrigTile;
-  unsigned ballots[kTrigPerThread];
+  for (int i = threadIdx.x; i < kSlots; i += kTrigThreads) s_cnt[i] = 0;
+  __syncthreads();
+  const double scale = kTrigBuckets / fmax(1.0 - thr, 1e-300);
+  int bkt[kTrigPerThread];
+  unsigned same[kTrigPerThread];
 #pragma unroll
   for (int i = 0; i < kTrigPerThread; ++i) {
     const long long c = tile0 + (long long)i * kTrigThreads + threadIdx.x;
-    bool f = false;
+    int b = -1;
     if (c < n) {
       const double sc = s[c];
       if (!is_finite(sc)) raise_failure(err_deep, c, 0, kFailActivity);
-      f = sc > thr;
+      if (sc > thr) b = min(kTrigBuckets - 1, max(0, (int)((sc - thr) * scale)));
     }
-    ballots[i] = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) s_cnt[i * 32 + warp] = __popc(ballots[i]);
+    bkt[i] = b;
+    same[i] = __match_any_sync(0xffffffffu, b);
+    if (b >= 0 && lane == __ffs(same[i]) - 1) s_cnt[(b * kTrigPerThread + i) * 32 + warp] = __popc(same[i]);
   }
   __syncthreads();
-  if (warp == 0) {
-    // exclusive scan of the 128 (i, warp) counts, in column order
-    int v[kTrigPerThread];
-    int tot = 0;
+  // block-wide exclusive scan of the kSlots counts (2 per thread)
+  const int e0 = 2 * threadIdx.x;
+  const int v0 = s_cnt[e0], v1 = s_cnt[e0 + 1];
+  int incl = v0 + v1;
 #pragma unroll
-    for (int i = 0; i < kTrigPerThread; ++i) { v[i] = s_cnt[lane * kTrigPerThread + i]; tot += v[i]; }
-    int incl = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = s_wsum[lane];
+    int wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
+      const int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
     }
-    int run = incl - tot;
-#pragma unroll
-    for (int i = 0; i < kTrigPerThread; ++i) { const int x = v[i]; s_cnt[lane * kTrigPerThread + i] = run; run += x; }
-    if (lane == 31) s_base = incl > 0 ? atomicAdd(count, incl) : 0;
+    s_wsum[lane] = wi - w;
+    if (lane == 31) s_base = wi > 0 ? atomicAdd(count, wi) : 0;
   }
+  __syncthreads();
+  const int excl = s_wsum[warp] + incl - (v0 + v1);
+  s_cnt[e0] = excl;
+  s_cnt[e0 + 1] = excl + v0;
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
   for (int i = 0; i < kTrigPerThread; ++i) {
-    if (ballots[i] & (1u << lane)) {
+    if (bkt[i] >= 0) {
       const long long c = tile0 + (long long)i * kTrigThreads + threadIdx.x;
-      idx[s_base + s_cnt[i * 32 + warp] + __popc(ballots[i] & lt)] = (int)c;
+      idx[s_base + s_cnt[(bkt[i] * kTrigPerThread + i) * 32 + warp] + __popc(same[i] & lt)] = (int)c;
     }
   }
 }
@@ -115,161 +140,279 @@ struct DeepArgs {
   long long ld_out;
   const int* idx;         // compacted triggered columns
   const int* count;       // number of triggered columns (device)
-  int* tile_cursor;       // persistent-block work cursor (zeroed per call)
+  unsigned long long* cursor;  // [0] work cursor (zeroed per call), [1..32] dummies
   unsigned long long* err;
   const double2* exp_tab; // 2^(j/512) double-double table (global)
   long long first_col;
   double thr, tol;
   int maxit;
   int L;                  // levels
-  int cpb;                // columns per tile
+  int batch;              // columns per precip batch (<= kDeepBatch)
   bool fast_div_ok;       // newton_tol >= 2^-500
 };
 
-template <int VAR>
-__device__ __forceinline__ double deep_exp(double x, const double2* tab, bool& fast) {
-  if (VAR == kVarApprox) {
-    fast = false;
-    return approx_exp_ref(x);
-  }
-  fast = exp_fast_ok(x);
-  return fast ? exp_tang(x, tab) : exp(x);
+// Deep-kernel lanes read a lane-private copy of the exp table (see
+// exp_tang); other kernels pass the plain table with kTabCopies = 1 views.
+constexpr int kTabCopies = 8;
+
+template <int VAR, int STRIDE = kTabCopies>
+__device__ __forceinline__ double deep_exp(double x, const double2* tab) {
+  if (VAR == kVarApprox) return approx_exp_ref(x);
+  return exp_fast_ok(x) ? exp_tang<STRIDE>(x, tab) : exp_cold(x);
 }
 
-// Inverse-entropy Newton iteration for one (y, guess) solve, restating
-// physics.cpp:64-87: up to max_iter+1 convergence tests, an update after
-// each failed test, non-finite iterates rejected.  The two solves of a lane
-// run as one flattened loop so a lane that converges its entrainment solve
-// moves straight on to its precipitation solve without waiting for its
-// warp.  Returns false on failure (raised into args.err).
+// Fast-path exp for |x| < 340 (caller checked exp_fast_ok): the table exp,
+// or approx_exp with its ldexp as an exact exponent add (|k| <= 491).
 template <int VAR>
-__device__ __forceinline__ bool deep_lane_solves(const DeepArgs& a, const double2* tab,
-                                                 long long col, int k, double ye, double yp,
-                                                 double guess, double e0, double c0,
-                                                 double& re, double& rp, int& work) {
-  const double tol = a.tol;
-  const int maxit = a.maxit;
-  const double kBig = 0x1.0p490;
-  const bool fastdiv0 =
-      a.fast_div_ok && fabs(ye) < kBig && fabs(yp) < kBig && exp_fast_ok(mul(kMC.c005, guess));
-  bool fastdiv = fastdiv0;
-  double y = ye, t = guess, e = e0, resid = sub(c0, ye);
-  int it = 0, pass = 0, order = k;
-  work = 0;
-  if (!is_finite(ye)) { raise_failure(a.err, col, order, kFailInput); return false; }
+__device__ __forceinline__ double deep_exp005_fast(double t, const double2* tab) {
+  if (VAR == kVarApprox) return approx_exp_ref_fast(mul(kMC.c005, t));
+  return exp005_tang<kTabCopies>(t, tab);
+}
+
+// Reference-faithful Newton loop (physics.cpp:64-87) continued from any
+// state, with every range check: convergence tested before each update, at
+// most max_iter updates, non-finite iterates rejected, IEEE division and
+// full-range exp.  `it` counts updates already taken.  Returns false on
+// failure (raised into a.err with the solve's reference order).
+template <int VAR>
+__device__ __forceinline__ bool newton_generic(const DeepArgs& a, const double2* tab, long long col,
+                                            int order, double y, double& t, double& e,
+                                            double& resid, int& it) {
   for (;;) {
-    if (it > maxit) { raise_failure(a.err, col, order, kFailNoConv); return false; }
-    if (fabs(resid) <= tol) {
-      work += it;
-      if (pass == 1) { rp = t; return true; }
-      re = t;
-      pass = 1;
-      order = a.L + k;
-      it = 0;
-      y = yp;
-      t = guess;
-      e = e0;
-      fastdiv = fastdiv0;
-      if (!is_finite(yp)) { raise_failure(a.err, col, order, kFailInput); return false; }
-      resid = sub(c0, yp);
-      continue;
-    }
+    if (it > a.maxit) { raise_failure(a.err, col, order, kFailNoConv); return false; }
+    if (fabs(resid) <= a.tol) return true;
     const double deriv = add(mul(kMC.c005, e), kMC.c001);
-    t = sub(t, fastdiv ? div_fast(resid, deriv) : div_rn(resid, deriv));
-    bool fast;
-    if (VAR == kVarApprox) {
-      if (!is_finite(t)) { raise_failure(a.err, col, order, kFailDiverged); return false; }
-      e = approx_exp_ref(mul(kMC.c005, t));
-      fast = false;
-    } else {
-      const double x = mul(kMC.c005, t);
-      fast = exp_fast_ok(x);
-      if (fast) {
-        e = exp_tang(x, tab);
-      } else {
-        if (!is_finite(t)) { raise_failure(a.err, col, order, kFailDiverged); return false; }
-        e = exp(x);
-      }
-    }
+    t = sub(t, div_rn(resid, deriv));
+    if (!is_finite(t)) { raise_failure(a.err, col, order, kFailDiverged); return false; }
+    e = deep_exp<VAR>(mul(kMC.c005, t), tab);
     resid = sub(add(e, mul(kMC.c001, t)), y);
-    fastdiv = fastdiv && fast;
     ++it;
   }
 }
 
+// Completes one solve: the common case (converged, within max_iter) inline,
+// anything else in the cold generic loop.
 template <int VAR>
-__global__ void __launch_bounds__(512, 2) deep_kernel(DeepArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* s_tab = reinterpret_cast<double2*>(smem_raw);                 // 512 x 16 B
-  double* s_term = reinterpret_cast<double*>(s_tab + kExpTableSize);      // cpb*L
-  int* s_work = reinterpret_cast<int*>(s_term + a.cpb * a.L);            // cpb*L
-  int* s_col = s_work + a.cpb * a.L;                                      // cpb
-  __shared__ int s_tile;
+__device__ __forceinline__ bool newton_finish(const DeepArgs& a, const double2* tab, long long col,
+                                              int order, double y, double& t, double& e, double& h,
+                                              int& it) {
+  if (it <= a.maxit && fabs(h) <= a.tol) return true;
+  return newton_generic<VAR>(a, tab, col, order, y, t, e, h, it);
+}
 
-  if (VAR != kVarApprox) {
-    for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
+// The lane's two solves -- entrainment (reference order k) and
+// precipitation (order L + k) of level k -- iterate in lockstep: two
+// independent dependency chains per lane (ILP 2) in one straight-line loop.
+// Within a column the two solves' iteration counts agree on ~99% of levels
+// (the guess is shared), so the loop runs while BOTH are unconverged and
+// hands whichever is left (usually nothing, at most an update or two) to
+// newton_finish.
+//
+// The fast loop carries no per-update range checks.  Its precondition P:
+//   newton_tol >= 2^-500, -60 < y < 2^490 for both solves, |0.05 guess| <
+//   340, and the guess right of both roots (initial residuals > 0).
+// f(t) = exp(0.05 t) + 0.01 t is increasing and convex, so Newton from the
+// right descends monotonically onto the root and never overshoots it (an FP
+// step's relative error ~1e-15 can only cross the root within ~1e-13 of
+// it); every iterate therefore lies in [root - tiny, guess].  y > -60 gives
+// root > 100 (y - 1) > -6100, so |0.05 t| < 340 throughout: exp_tang's
+// domain.  Then every derivative 0.05 e + 0.01 lies in [0.01, 2^488) and
+// every residual divided (only while |r| > tol) in (2^-500, 2^500): the
+// operand range where div_fast is exact.  Inputs outside P take the
+// reference-faithful generic loop from the start.  Semantics per solve are
+// exactly the reference's; a failure in one solve does not stop the other
+// (the reference reports the first failure in its own solve order,
+// recovered from the failure key).
+template <int VAR>
+__device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2* tab, long long col,
+                                               int k, double ye, double yp, double guess, double e0,
+                                               double c0, double& re, double& rp, int& work) {
+  const double kBig = 0x1.0p490;
+  double te = guess, ee = e0, he = sub(c0, ye);
+  double tp = guess, ep = e0, hp = sub(c0, yp);
+  int it = 0;
+  const bool inputs_ok = is_finite(ye) && is_finite(yp);
+  const bool fast_ok = inputs_ok && a.fast_div_ok && ye > -60.0 && yp > -60.0 && ye < kBig &&
+                       yp < kBig && he > 0.0 && hp > 0.0 && exp_fast_ok(mul(kMC.c005, guess));
+  if (fast_ok) {
+    const double tol = a.tol;
+    const int maxit = a.maxit;
+    while (it <= maxit) {
+      if (abs_le(he, tol) || abs_le(hp, tol)) break;   // tol >= 2^-500 here
+      te = sub(te, div_fast(he, add(mul(kMC.c005, ee), kMC.c001)));
+      tp = sub(tp, div_fast(hp, add(mul(kMC.c005, ep), kMC.c001)));
+      ee = deep_exp005_fast<VAR>(te, tab);
+      ep = deep_exp005_fast<VAR>(tp, tab);
+      he = sub(add(ee, mul(kMC.c001, te)), ye);
+      hp = sub(add(ep, mul(kMC.c001, tp)), yp);
+      ++it;
+    }
   }
-  const int L = a.L, cpb = a.cpb;
-  const int lanes = cpb * L;
-  const int lc = threadIdx.x / L, k = threadIdx.x - (threadIdx.x / L) * L;
+  int ie = it, ip = it;
+  bool ok = true;
+  if (!inputs_ok) {
+    if (!is_finite(ye)) { raise_failure(a.err, col, k, kFailInput); ok = false; }
+    else if (!newton_generic<VAR>(a, tab, col, k, ye, te, ee, he, ie)) ok = false;
+    if (!is_finite(yp)) { raise_failure(a.err, col, a.L + k, kFailInput); ok = false; }
+    else if (!newton_generic<VAR>(a, tab, col, a.L + k, yp, tp, ep, hp, ip)) ok = false;
+  } else {
+    if (!newton_finish<VAR>(a, tab, col, k, ye, te, ee, he, ie)) ok = false;
+    if (!newton_finish<VAR>(a, tab, col, a.L + k, yp, tp, ep, hp, ip)) ok = false;
+  }
+  re = te;
+  rp = tp;
+  work = ie + ip;
+  return ok;
+}
+
+// One warp per triggered column, lane k = level k (levels k, k+32, ... when
+// L > 32).  A column's 60 solves share the guess, so their iteration counts
+// agree almost everywhere and the warp runs converged (0.03 mean spread);
+// the trigger kernel's s-bucketing keeps a warp's consecutive entries at
+// near-equal work, and warps never wait on a block barrier.  Per-column scalars are finished in batches: each column's
+// precipitation terms are parked in shared memory and, every kBatch
+// columns, lane i sums column i's terms in k order (physics.cpp:161) -- one
+// warp instruction serves kBatch columns instead of one.
+constexpr int kDeepBatch = 16;
+constexpr int kDeepChunk = 4;   // list entries claimed per atomic (power of 2)
+
+// The deep role of a warp: walks the compacted list until it is exhausted.
+// s_tab points at this lane's copy of the replicated exp table; s_term is
+// this warp's [batch][L] precip scratch, s_bcol / s_bwork its batch slots.
+template <int VAR, bool NARROW>
+__device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_tab, double* s_term,
+                                            int* s_bcol, int* s_bwork, int lane) {
+  const int L = a.L;
   const long long A = *a.count;
   const bool reduced = (VAR == kVarReduced);
-
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_cursor, 1);
-    __syncthreads();
-    const long long first = (long long)s_tile * cpb;
-    if (first >= A) break;
-    if (threadIdx.x < cpb) s_col[threadIdx.x] = (first + threadIdx.x < A) ? a.idx[first + threadIdx.x] : -1;
-    __syncthreads();
-
-    double term = 0.0;
+  // Work distribution: warps claim aligned chunks of kDeepChunk list
+  // entries from a global cursor (one atomic per chunk), so SMs finish
+  // together whatever the per-column cost mix (cluster intensity varies
+  // across the grid).  Two-deep software pipeline: an entry's (s, T[lane],
+  // q[lane]) are loaded during the previous entry's solves, the entry after
+  // next is known a column ahead, and the next chunk is claimed a chunk
+  // ahead, so no load or atomic sits on the issue path of a column.
+  // Every lane issues the claim atomic -- lane 0 on the cursor, the others
+  // adding 0 to private dummy words -- so the addresses are not uniform and
+  // ptxas does not turn it into a warp-aggregated atomic, whose result
+  // broadcast (SHFL) would wait for the atomic right away.
+  long long next_raw = 0;
+  auto claim = [&]() {
+    unsigned long long* addr = lane == 0 ? a.cursor : a.cursor + 1 + lane;
+    const unsigned long long inc = lane == 0 ? (unsigned long long)kDeepChunk : 0ULL;
+    next_raw = (long long)atomicAdd(addr, inc);
+  };
+  auto advance = [&](long long x) -> long long {
+    if (((x + 1) & (kDeepChunk - 1)) != 0) return x + 1;
+    const long long r = __shfl_sync(0xffffffffu, next_raw, 0);
+    claim();
+    return r;
+  };
+  claim();
+  long long j = __shfl_sync(0xffffffffu, next_raw, 0);
+  claim();
+  long long jn = advance(j);
+  int c = 0, cn = 0;
+  double s_c = 0.0, T_c = 0.0, q_c = 0.0;
+  if (j < A) {
+    c = a.idx[j];
+    if (jn < A) cn = a.idx[jn];
+    s_c = a.s[c];
+    if (NARROW && lane < L) {
+      T_c = a.T[(long long)lane * a.ld_in + c];
+      q_c = a.q[(long long)lane * a.ld_in + c];
+    }
+  }
+  int nb = 0;  // columns parked in the batch
+  while (j < A) {
+    const long long jnn = (jn < A) ? advance(jn) : A;
+    const int cnn = (jnn < A) ? a.idx[jnn] : 0;
+    const double sc = s_c;
+    // physics.cpp:121 / :127 / :146
+    const double guess = add(24.0, mul(160.0, sc));
+    const double rho = add(1.0, mul(kMC.c005, sc));
+    const double e0 = deep_exp<VAR>(mul(kMC.c005, guess), s_tab);
+    const double c0 = add(e0, mul(kMC.c001, guess));
+    const long long col = a.first_col + c;
     int wl = 0;
-    const int c = (threadIdx.x < lanes) ? s_col[lc] : -1;
-    if (c >= 0) {
-      const double sc = a.s[c];
-      const double T = a.T[(long long)k * a.ld_in + c];
-      const double q = a.q[(long long)k * a.ld_in + c];
-      // physics.cpp:121 / :127 / :146-148 / :155-156
-      const double guess = add(24.0, mul(160.0, sc));
-      const double rho = add(1.0, mul(kMC.c005, sc));
-      const double m = reduced ? div_rn(q, mul(rho, rho)) : div_rn(div_rn(q, rho), rho);
+    bool ok_all = true;
+    // NARROW (L <= 32): one level per lane, its (T, q) prefetched; wide
+    // columns loop over levels lane, lane + 32, ... with plain loads (kept in
+    // a separate instantiation: a conditional load sharing a scoreboard slot
+    // with the prefetch would stall every column on the prefetch)
+    for (int k = lane; k < L; k += 32) {
+      double T, q;
+      if (NARROW) {
+        T = T_c;
+        q = q_c;
+        if (jn < A) {  // prefetch the next entry behind the solves
+          s_c = a.s[cn];
+          T_c = a.T[(long long)lane * a.ld_in + cn];
+          q_c = a.q[(long long)lane * a.ld_in + cn];
+        }
+      } else {
+        T = a.T[(long long)k * a.ld_in + c];
+        q = a.q[(long long)k * a.ld_in + c];
+        if (k == lane && jn < A) s_c = a.s[cn];
+      }
+      double m;  // physics.hpp:94-96 via the shared-divisor form of div_rn
+      {
+        const double dv = reduced ? mul(rho, rho) : rho;
+        if (div_operand_ok(dv) && div_operand_ok(q)) {
+          const double ydv = rcp_refined(dv);
+          m = div_by(q, dv, ydv);
+          if (!reduced) m = div_operand_ok(m) ? div_by(m, dv, ydv) : div_rn(m, dv);
+        } else {
+          m = reduced ? div_rn(q, dv) : div_rn(div_rn(q, rho), rho);
+        }
+      }
+      // physics.cpp:147-148 / :156-157
       const double ye = add(add(1.0, mul(1.0e-3, T)), mul(0.1, m));
       const double yp = add(add(add(1.0, mul(8.0e-4, T)), mul(kMC.c005, m)), mul(0.1, sc));
-      bool f0;
-      const double e0 = deep_exp<VAR>(mul(kMC.c005, guess), s_tab, f0);
-      const double c0 = add(e0, mul(kMC.c001, guess));
       double re = 0.0, rp = 0.0;
-      const long long col = a.first_col + c;
-      if (deep_lane_solves<VAR>(a, s_tab, col, k, ye, yp, guess, e0, c0, re, rp, wl)) {
+      int w = 0;
+      double term = 0.0;
+      if (deep_lane_pair<VAR>(a, s_tab, col, k, ye, yp, guess, e0, c0, re, rp, w)) {
         // physics.cpp:151-152 / :159-161
+        double sin_a, sin_b;
+        sin2_cw(add(mul(6.0, T), mul(50.0, q)), mul(3.0, rp), sin_a, sin_b);
         const long long o = (long long)k * a.ld_out + c;
-        a.tend_T[o] = add(mul(0.02, sub(add(250.0, mul(2.0, re)), T)),
-                          mul(0.3, sin(add(mul(6.0, T), mul(50.0, q)))));
-        a.tend_q[o] = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, sin(mul(3.0, rp)))), q));
+        a.tend_T[o] = add(mul(0.02, sub(add(250.0, mul(2.0, re)), T)), mul(0.3, sin_a));
+        a.tend_q[o] = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, sin_b)), q));
         term = mul(q, max0(sub(rp, 4.5)));
+      } else {
+        ok_all = false;
       }
+      s_term[nb * L + k] = term;
+      wl += w;
     }
-    if (threadIdx.x < lanes) {
-      s_term[threadIdx.x] = term;
-      s_work[threadIdx.x] = wl;
+    const int wsum = __reduce_add_sync(0xffffffffu, wl);
+    const bool ok = __all_sync(0xffffffffu, ok_all);
+    if (lane == 0) {
+      s_bcol[nb] = ok ? c : -1;
+      s_bwork[nb] = wsum;
     }
-    __syncthreads();
-    if (threadIdx.x < cpb) {
-      const int cc = s_col[threadIdx.x];
-      if (cc >= 0) {
-        double pr = 0.0;  // ordered k sum, physics.cpp:161
-        long long w = 0;
-        for (int kk = 0; kk < L; ++kk) {
-          pr = add(pr, s_term[threadIdx.x * L + kk]);
-          w += s_work[threadIdx.x * L + kk];
+    ++nb;
+    c = cn;
+    cn = cnn;
+    j = jn;
+    jn = jnn;
+    if (nb == a.batch || j >= A) {
+      __syncwarp();
+      if (lane < nb) {
+        const int cc = s_bcol[lane];
+        if (cc >= 0) {
+          double pr = 0.0;  // ordered k sum, physics.cpp:161
+          const double* t = s_term + lane * L;
+          for (int kk = 0; kk < L; ++kk) pr = add(pr, t[kk]);
+          a.precip[cc] = pr;
+          a.work[cc] = s_bwork[lane];
+          a.exited[cc] = 0;
         }
-        a.precip[cc] = pr;
-        a.work[cc] = w;
-        a.exited[cc] = 0;
       }
+      __syncwarp();
+      nb = 0;
     }
-    __syncthreads();
   }
 }
 
@@ -306,18 +449,35 @@ struct ShallowArgs {
   int L;
 };
 
-template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO>
-__global__ void __launch_bounds__(256) shallow_kernel(ShallowArgs a) {
-  __shared__ double2 s_tab[kExpTableSize];
-  if (DO_SHALLOW && VAR != kVarApprox) {
-    for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
-    __syncthreads();
-  }
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= a.n) return;
+// One column of the shallow scheme (and/or the deep zero-fill), one thread.
+// STRIDE: exp table layout (1 = plain, kTabCopies = replicated, lane copy).
+// The level loop runs in chunks of kShChunk with the chunk's loads issued
+// before any use, so each thread keeps 2 kShChunk loads in flight.
+constexpr int kShChunk = 5;
+
+// Where a column's (T[k], q[k]) come from: global rows (stride ld) or a
+// shared-memory tile (stride = tile width).
+struct GlobalRows {
+  const double* T;
+  const double* q;
+  long long ld;
+  __device__ __forceinline__ double t(int k) const { return T[(long long)k * ld]; }
+  __device__ __forceinline__ double m(int k) const { return q[(long long)k * ld]; }
+};
+struct SmemRows {
+  const double* T;
+  const double* q;
+  int ld;
+  __device__ __forceinline__ double t(int k) const { return T[k * ld]; }
+  __device__ __forceinline__ double m(int k) const { return q[k * ld]; }
+};
+
+template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO, int STRIDE, class SRC>
+__device__ __forceinline__ void shallow_column_src(const ShallowArgs& a, long long c, double sc,
+                                                   const SRC& src, const double2* tab) {
   const int L = a.L;
-  const double sc = a.s[c];
   if (DO_DEEP_ZERO && !(sc > a.thr)) {
+#pragma unroll 10
     for (int k = 0; k < L; ++k) {
       a.d_tend_T[(long long)k * a.d_ld_out + c] = 0.0;
       a.d_tend_q[(long long)k * a.d_ld_out + c] = 0.0;
@@ -336,19 +496,42 @@ __global__ void __launch_bounds__(256) shallow_kernel(ShallowArgs a) {
   const bool reduced = (VAR == kVarReduced);
   const double rho = add(1.0, mul(kMC.c005, sc));
   const double rho2 = mul(rho, rho);
+  // the per-level divisions share one divisor: its reciprocal is refined
+  // once per column (div_by == div_fast bit for bit)
+  const double dv = reduced ? rho2 : rho;
+  const bool dv_ok = div_operand_ok(dv);
+  const double ydv = rcp_refined(dv);
   double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-  for (int k = 0; k < L; ++k) {
-    const double T = a.T[(long long)k * a.ld_in + c];
-    const double q = a.q[(long long)k * a.ld_in + c];
-    const double m = reduced ? div_rn(q, rho2) : div_rn(div_rn(q, rho), rho);
-    const double x = mul(-50.0, q);
-    double ex;
-    if (VAR == kVarApprox) ex = approx_exp_ref(x);
-    else ex = exp_fast_ok(x) ? exp_tang(x, s_tab) : exp(x);
-    p0 = add(p0, add(mul(a1_0, T), mul(30.0, m)));
-    p1 = add(p1, add(add(mul(a1_1, T), mul(20.0, m)), mul(0.02, ex)));
-    p2 = add(p2, add(mul(a1_2, T), mul(40.0, m)));
-    p3 = add(p3, add(mul(a1_3, T), mul(25.0, m)));
+  for (int k0 = 0; k0 < L; k0 += kShChunk) {
+    double Tk[kShChunk], qk[kShChunk];
+#pragma unroll
+    for (int i = 0; i < kShChunk; ++i) {
+      const int k = k0 + i;
+      if (k < L) {
+        Tk[i] = src.t(k);
+        qk[i] = src.m(k);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kShChunk; ++i) {
+      if (k0 + i >= L) break;
+      const double T = Tk[i], q = qk[i];
+      double m;
+      if (dv_ok && div_operand_ok(q)) {
+        m = div_by(q, dv, ydv);
+        if (!reduced) m = div_operand_ok(m) ? div_by(m, dv, ydv) : div_rn(m, dv);
+      } else {
+        m = reduced ? div_rn(q, rho2) : div_rn(div_rn(q, rho), rho);
+      }
+      const double x = mul(-50.0, q);
+      double ex;
+      if (VAR == kVarApprox) ex = approx_exp_ref(x);
+      else ex = exp_fast_ok(x) ? exp_tang<STRIDE>(x, tab) : exp_cold(x);
+      p0 = add(p0, add(mul(a1_0, T), mul(30.0, m)));
+      p1 = add(p1, add(add(mul(a1_1, T), mul(20.0, m)), mul(0.02, ex)));
+      p2 = add(p2, add(mul(a1_2, T), mul(40.0, m)));
+      p3 = add(p3, add(mul(a1_3, T), mul(25.0, m)));
+    }
   }
   const double dl = (double)L;
   const double ps[4] = {p0, p1, p2, p3};
@@ -361,11 +544,12 @@ __global__ void __launch_bounds__(256) shallow_kernel(ShallowArgs a) {
   for (int j = 0; j < 4; ++j) {
     acc = add(acc, add(div_rn(ps[j], dl), mul(w3[j], sc)));
     ++phases;
-    const double lhs = mul(sc, add(1.0, mul(kMC.c005, sin(mul(3.0, acc)))));
+    const double lhs = mul(sc, add(1.0, mul(kMC.c005, sin_cw(mul(3.0, acc)))));
     if (lhs < theta[j]) { survived = false; break; }
   }
   a.work[c] = (long long)phases * L;
   if (!survived) {
+#pragma unroll 10
     for (int k = 0; k < L; ++k) {
       a.tend_T[(long long)k * a.ld_out + c] = 0.0;
       a.tend_q[(long long)k * a.ld_out + c] = 0.0;
@@ -374,16 +558,211 @@ __global__ void __launch_bounds__(256) shallow_kernel(ShallowArgs a) {
     a.exited[c] = 1;
     return;
   }
-  const double sa = sin(acc);
+  const double sa = sin_cw(acc);
   const double base = add(256.0, mul(2.0, sa));
+#pragma unroll 10
   for (int k = 0; k < L; ++k) {
-    const double T = a.T[(long long)k * a.ld_in + c];
-    const double q = a.q[(long long)k * a.ld_in + c];
+    const double T = src.t(k);
+    const double q = src.m(k);
     a.tend_T[(long long)k * a.ld_out + c] = mul(0.005, sub(base, T));
     a.tend_q[(long long)k * a.ld_out + c] = mul(0.02, sub(0.012, q));
   }
   a.precip[c] = mul(sub(sc, 0.5), max0(add(sa, 0.5)));
   a.exited[c] = 0;
+}
+
+template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO, int STRIDE>
+__device__ __forceinline__ void shallow_column(const ShallowArgs& a, long long c, const double2* tab) {
+  shallow_column_src<VAR, DO_SHALLOW, DO_DEEP_ZERO, STRIDE>(a, c, a.s[c], GlobalRows{a.T + c, a.q + c, a.ld_in},
+                                                            tab);
+}
+
+constexpr int kShallowThreads = 128;
+
+// Standalone shallow(+zero-fill) kernel: one thread per column.
+template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO>
+__global__ void __launch_bounds__(kShallowThreads, 8) shallow_kernel(ShallowArgs a) {
+  __shared__ double2 s_tab[kExpTableSize];
+  if (DO_SHALLOW && VAR != kVarApprox) {
+    for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
+    __syncthreads();
+  }
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.n) return;
+  shallow_column<VAR, DO_SHALLOW, DO_DEEP_ZERO, 1>(a, c, s_tab);
+}
+
+// ---------------------------------------------------------------------------
+// Streaming shallow(+zero-fill) kernel, L2-prefetched: persistent blocks of
+// kShTile threads walk tiles of kShTile columns (a thread per column,
+// registers-only, 8 blocks per SM); while a block computes tile t, one lane
+// asks the TMA engine to prefetch tile t + G's 2 L rows into L2, so the
+// per-thread row loads of the next tile are L2 hits instead of HBM round
+// trips.  No shared-memory staging: occupancy stays at 32 warps/SM for the
+// per-column serial chains (the ordered level sums, physics.cpp:183-204).
+template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO>
+__global__ void __launch_bounds__(128, 8) shallow_stream_kernel(ShallowArgs a) {
+  __shared__ double2 s_tab[kExpTableSize];
+  if (DO_SHALLOW && VAR != kVarApprox) {
+    for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
+  }
+  __syncthreads();
+  const int L = a.L;
+  const long long ntiles = (a.n + 127) / 128;
+  auto prefetch = [&](long long tile) {
+    const long long c0 = tile * 128;
+    const long long cols = min(128LL, a.n - c0);
+    const unsigned bytes = (unsigned)(((cols * 8) + 15) & ~15LL);
+    const bool ok = ((a.ld_in & 1) == 0) && (c0 + (bytes / 8) <= a.ld_in);
+    if (!ok) return;
+    for (int k = (int)threadIdx.x; k < 2 * L; k += blockDim.x) {
+      const double* base = (k < L ? a.T + (long long)k * a.ld_in : a.q + (long long)(k - L) * a.ld_in) + c0;
+      bulk_prefetch_l2(base, bytes);
+    }
+  };
+  long long tile = blockIdx.x;
+  if (DO_SHALLOW && tile < ntiles) prefetch(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    if (DO_SHALLOW && tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
+    const long long c = tile * 128 + threadIdx.x;
+    if (c < a.n) shallow_column<VAR, DO_SHALLOW, DO_DEEP_ZERO, 1>(a, c, s_tab);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Streaming shallow(+zero-fill) kernel on the TMA engine: one persistent
+// block per SM walks tiles of kShTile columns; thread 0 stages the next
+// tile's 2L rows (T and q, 1 KB each) into the idle half of a double buffer
+// with cp.async.bulk while the block computes the current tile out of
+// shared memory, so every SM keeps a whole tile (2 L KB) of loads in flight
+// without registers, and the survivors' output pass re-reads T, q from
+// shared memory instead of HBM.  Requires ld_in % 2 == 0 (16-byte aligned
+// rows); the tail (n % kShTile columns) is done from global by block 0.
+constexpr int kShTile = 128;
+
+template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO>
+__global__ void __launch_bounds__(kShTile, 1) shallow_tma_kernel(ShallowArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t s_bar[2];
+  double2* s_tab = reinterpret_cast<double2*>(smem_raw);                       // 8 KB
+  double* buf = reinterpret_cast<double*>(smem_raw + kExpTableSize * sizeof(double2));
+  const int L = a.L;
+  const int tid = threadIdx.x;
+  const size_t stage_elems = (size_t)2 * L * kShTile;   // T then q, [L][kShTile] each
+  const long long ntiles = a.n / kShTile;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  if (DO_SHALLOW && VAR != kVarApprox) {
+    for (int i = tid; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
+  }
+  __syncthreads();
+  auto issue = [&](long long tile, int stage) {
+    double* dT = buf + stage * stage_elems;
+    double* dq = dT + (size_t)L * kShTile;
+    const long long c0 = tile * kShTile;
+    mbar_arrive_expect_tx(&s_bar[stage], (unsigned)(2 * L * kShTile * sizeof(double)));
+    for (int k = 0; k < L; ++k) {
+      bulk_g2s(dT + k * kShTile, a.T + (long long)k * a.ld_in + c0, kShTile * sizeof(double), &s_bar[stage]);
+      bulk_g2s(dq + k * kShTile, a.q + (long long)k * a.ld_in + c0, kShTile * sizeof(double), &s_bar[stage]);
+    }
+  };
+  long long tile = blockIdx.x;
+  if (DO_SHALLOW && tid == 0 && tile < ntiles) issue(tile, 0);
+  for (int i = 0; tile < ntiles; ++i, tile += gridDim.x) {
+    const int stage = i & 1;
+    const long long nxt = tile + gridDim.x;
+    if (DO_SHALLOW && tid == 0 && nxt < ntiles) issue(nxt, stage ^ 1);
+    const long long c = tile * kShTile + tid;
+    const double sc = a.s[c];
+    if (DO_SHALLOW) {
+      mbar_wait_parity(&s_bar[stage], (unsigned)((i >> 1) & 1));
+      const double* sT = buf + stage * stage_elems + tid;
+      shallow_column_src<VAR, true, DO_DEEP_ZERO, 1>(a, c, sc, SmemRows{sT, sT + (size_t)L * kShTile, kShTile},
+                                                     s_tab);
+    } else {
+      shallow_column_src<VAR, false, DO_DEEP_ZERO, 1>(a, c, sc, GlobalRows{a.T + c, a.q + c, a.ld_in}, s_tab);
+    }
+    __syncthreads();  // stage fully consumed before it is refilled
+  }
+  if (blockIdx.x == 0) {
+    for (long long c = ntiles * kShTile + tid; c < a.n; c += blockDim.x)
+      shallow_column<VAR, DO_SHALLOW, DO_DEEP_ZERO, 1>(a, c, s_tab);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused persistent convection kernel: one block per SM, kFusedWarps warps.
+// The deep plume is FP64-bound and the shallow scheme + deep zero-fill
+// HBM-bound, so one kernel runs both at once by warp specialisation:
+// warps [0, n_col_warps) first stream column tiles (32 columns, a thread
+// per column) for the shallow scheme and the zero-fill, claiming tiles from
+// a global cursor; the remaining warps -- and the column warps once the
+// tiles run out -- work the deep list.  The block's shared memory holds the
+// exp table replicated kTabCopies times (bank-conflict-free lookups) and
+// each warp's deep precip batch.
+constexpr int kFusedWarps = 24;
+
+// Standalone deep kernel (split mode): every warp of the persistent block
+// works the deep list.
+template <int VAR, bool NARROW>
+__global__ void __launch_bounds__(kFusedWarps * 32, 1) deep_kernel(DeepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_bcol[kFusedWarps][kDeepBatch];
+  __shared__ int s_bwork[kFusedWarps][kDeepBatch];
+  double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
+  if (VAR != kVarApprox) {
+    for (int i = threadIdx.x; i < kExpTableSize * kTabCopies; i += blockDim.x)
+      s_tab_all[i] = a.exp_tab[i / kTabCopies];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const double2* s_tab = s_tab_all + (lane & (kTabCopies - 1));
+  double* s_term = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies) +
+                   (size_t)wib * a.batch * a.L;
+  deep_worker<VAR, NARROW>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], lane);
+}
+
+template <int VAR, bool NARROW, bool DO_SH, bool DO_DEEP>
+__global__ void __launch_bounds__(kFusedWarps * 32, 1)
+convect_kernel(DeepArgs a, ShallowArgs b, int n_col_warps, unsigned long long* tile_cursor) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_bcol[kFusedWarps][kDeepBatch];
+  __shared__ int s_bwork[kFusedWarps][kDeepBatch];
+  double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
+  if (VAR != kVarApprox) {
+    for (int i = threadIdx.x; i < kExpTableSize * kTabCopies; i += blockDim.x)
+      s_tab_all[i] = a.exp_tab[i / kTabCopies];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const double2* s_tab = s_tab_all + (lane & (kTabCopies - 1));
+  if ((DO_SH || DO_DEEP) && wib < n_col_warps) {
+    // column-stream role; the next tile is claimed a tile ahead (every lane
+    // issues the atomic so it is not warp-aggregated, see deep_worker)
+    const long long ntiles = (b.n + 31) / 32;
+    long long next_raw = 0;
+    auto claim = [&]() {
+      unsigned long long* addr = lane == 0 ? tile_cursor : tile_cursor + 1 + lane;
+      next_raw = (long long)atomicAdd(addr, lane == 0 ? 1ULL : 0ULL);
+    };
+    claim();
+    long long tile = __shfl_sync(0xffffffffu, next_raw, 0);
+    claim();
+    while (tile < ntiles) {
+      const long long c = tile * 32 + lane;
+      if (c < b.n) shallow_column<VAR, DO_SH, DO_DEEP, kTabCopies>(b, c, s_tab);
+      tile = __shfl_sync(0xffffffffu, next_raw, 0);
+      claim();
+    }
+  }
+  if (DO_DEEP) {
+    double* s_term = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies) +
+                     (size_t)wib * a.batch * a.L;
+    deep_worker<VAR, NARROW>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], lane);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -402,16 +781,15 @@ __global__ void ientropy_kernel(const double* __restrict__ y, const double* __re
   if (i >= n) return;
   const double yy = y[i], guess = g[i];
   if (!is_finite(yy) || !is_finite(guess)) { raise_failure(err, i, 0, kFailInput); return; }
-  bool f;
   double t = guess;
-  double e = deep_exp<VAR>(mul(kMC.c005, t), s_tab, f);
+  double e = deep_exp<VAR, 1>(mul(kMC.c005, t), s_tab);
   double resid = sub(add(e, mul(kMC.c001, t)), yy);
   for (int it = 0; it <= maxit; ++it) {
     if (fabs(resid) <= tol) { root[i] = t; iters[i] = it; return; }
     const double deriv = add(mul(kMC.c005, e), kMC.c001);
     t = sub(t, div_rn(resid, deriv));
     if (!is_finite(t)) { raise_failure(err, i, 0, kFailDiverged); return; }
-    e = deep_exp<VAR>(mul(kMC.c005, t), s_tab, f);
+    e = deep_exp<VAR, 1>(mul(kMC.c005, t), s_tab);
     resid = sub(add(e, mul(kMC.c001, t)), yy);
   }
   raise_failure(err, i, 0, kFailNoConv);
