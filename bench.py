@@ -250,14 +250,10 @@ def run_gpu_arm(args):
     L, n_total = T.shape
     opts = P.KernelOptions(variant=args.variant, activity_threshold=thr)
 
-    # partition: contiguous ranges balanced by estimated cost
+    # partition: contiguous ranges balanced by estimated cost (multigpu.py)
+    from paper_1711_00289_b200 import multigpu
     hbm_gbs, hbm_src = measured_peaks()
-    deep_w = 159.0 * L + 37.0 * 694.0               # FLOP model, mean U at guess 24+160s
-    shallow_w = 1482.0 * (34.0e12 / (hbm_gbs * 1e9))  # bytes priced at the FP64/HBM ratio
-    if args.partition == "naive":
-        bounds = P.plan_partition(s, thr, ws, 0.0, 1.0)
-    else:
-        bounds = P.plan_partition(s, thr, ws, deep_w, shallow_w)
+    bounds = multigpu.rank_bounds(s, thr, ws, args.partition, L, hbm_gbs)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     n = hi - lo
     s_r, T_r, q_r = s[lo:hi], np.ascontiguousarray(T[:, lo:hi]), np.ascontiguousarray(q[:, lo:hi])

@@ -709,7 +709,7 @@ constexpr int kFusedWarps = 24;
 // works the deep list.
 template <int VAR, bool NARROW>
 __global__ void __launch_bounds__(kFusedWarps * 32, 1) deep_kernel(DeepArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ int s_bcol[kFusedWarps][kDeepBatch];
   __shared__ int s_bwork[kFusedWarps][kDeepBatch];
   double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) deep_kernel(DeepArgs a) {
 template <int VAR, bool NARROW, bool DO_SH, bool DO_DEEP>
 __global__ void __launch_bounds__(kFusedWarps * 32, 1)
 convect_kernel(DeepArgs a, ShallowArgs b, int n_col_warps, unsigned long long* tile_cursor) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ int s_bcol[kFusedWarps][kDeepBatch];
   __shared__ int s_bwork[kFusedWarps][kDeepBatch];
   double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
