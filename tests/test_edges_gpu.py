@@ -1,0 +1,171 @@
+"""GPU tier: error semantics and edge cases at the C ABI, checked against the
+reference's behaviour (the serial driver's first -- i.e. lowest -- failing
+column, physics.cpp:227-245; KernelError taxonomy, errors.hpp:26-36,
+capi.cpp:51-81) and against the oracle for ragged/odd shapes."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1711_00289_b200 as P
+from paper_1711_00289_b200 import gridgen as G
+
+pytestmark = pytest.mark.gpu
+
+
+def both_close(got, want):
+    for f, g in (("tend_T", "tend_T"), ("tend_q", "tend_q"), ("precip", "precip")):
+        a, b = getattr(got, f), getattr(want, g)
+        assert (np.abs(a - b) <= np.maximum(1e-10 * np.abs(b), 1e-14)).all(), f
+    assert np.array_equal(got.exited_early, want.exited)
+
+
+def test_kernel_error_reports_lowest_column(ctx):
+    # test_physics.cpp:488-501: NaN T in active column 5 -> KernelError column 5
+    s, T, q = O.make_grid(8, 30, 1.0, 42)
+    T[3, 5] = np.nan
+    with pytest.raises(P.KernelError) as e:
+        ctx.deep_convection(s, T, q)
+    assert e.value.column == 5 and "column 5" in str(e.value) and "non-finite input" in str(e.value)
+    # several failing columns: the lowest is reported
+    T[7, 2] = np.nan
+    T[0, 7] = np.inf
+    with pytest.raises(P.KernelError) as e:
+        ctx.deep_convection(s, T, q)
+    assert e.value.column == 2
+    # first_col offsets the reported id (ColumnState::col_id)
+    with pytest.raises(P.KernelError) as e:
+        ctx.deep_convection(s, T, q, first_col=1000)
+    assert e.value.column == 1002
+
+
+def test_nan_activity_fails_both_kernels(ctx):
+    s, T, q = G.make_config("c1", n=256, seed=1)
+    s[100] = np.nan
+    s[200] = np.inf
+    for kern in ("deep_convection", "shallow_convection"):
+        with pytest.raises(P.KernelError) as e:
+            getattr(ctx, kern)(s, T, q)
+        assert e.value.column == 100 and "non-finite activity" in str(e.value)
+
+
+def test_nan_moisture_in_inactive_deep_column_is_not_an_error(ctx):
+    # deep throws on NaN T/q only for active columns (physics.cpp:111-113)
+    s, T, q = O.make_grid(64, 30, 0.3, 7)
+    inactive = int(np.nonzero(s <= 0.5)[0][0])
+    q[4, inactive] = np.nan
+    deep = ctx.deep_convection(s, T, q)
+    od = O.convection("deep", s, T, q)
+    assert od.status == 0
+    both_close(deep, od)
+    # shallow propagates NaN into outputs without failing (predicate false)
+    sh = ctx.shallow_convection(s, T, q)
+    osh = O.convection("shallow", s, T, q)
+    assert osh.status == 0
+    assert np.array_equal(sh.exited_early, osh.exited) and np.array_equal(sh.work_units, osh.work)
+    assert np.array_equal(np.isnan(sh.tend_T), np.isnan(osh.tend_T))
+
+
+def test_max_iter_exceeded_is_no_convergence(ctx):
+    # test_physics.cpp:223-224 (max_iter = 2), at batch level
+    s, T, q = O.make_grid(16, 30, 0.5, 3)
+    opts = P.KernelOptions(newton_max_iter=2)
+    with pytest.raises(P.KernelError) as e:
+        ctx.deep_convection(s, T, q, opts)
+    od = O.convection("deep", s, T, q, O.Options(newton_max_iter=2))
+    assert od.status == 4 and e.value.column == od.fail_col
+    assert "no convergence within 2 iterations" in str(e.value)
+    with pytest.raises(P.KernelError):
+        ctx.ientropy_solve([1.3], [184.0], opts)
+
+
+def test_exact_max_iter_boundary(ctx):
+    # a solve needing exactly U updates passes with max_iter = U and fails with U - 1
+    st, root, it, _ = O.ientropy_solve(1.3, 184.0)
+    r, i = ctx.ientropy_solve([1.3], [184.0], P.KernelOptions(newton_max_iter=it))
+    assert i[0] == it
+    with pytest.raises(P.KernelError):
+        ctx.ientropy_solve([1.3], [184.0], P.KernelOptions(newton_max_iter=it - 1))
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 33, 4095, 4097, 12345])
+def test_ragged_sizes(ctx, n):
+    s, T, q = G.make_config("ref", n=max(n, 1), seed=n + 1)
+    s, T, q = s[:n], np.ascontiguousarray(T[:, :n]), np.ascontiguousarray(q[:, :n])
+    deep, sh = ctx.convect(s, T, q)
+    if n == 0:
+        assert deep.tend_T.shape == (30, 0)
+        return
+    both_close(deep, O.convection("deep", s, T, q))
+    both_close(sh, O.convection("shallow", s, T, q))
+
+
+@pytest.mark.parametrize("L", [1, 7, 30, 32, 33, 64])
+def test_level_counts(ctx, L):
+    s, T, q = G.make_config("ref", n=700, L=L, seed=L)
+    for v in (0, 2):
+        deep, sh = ctx.convect(s, T, q, P.KernelOptions(variant=v))
+        oo = O.Options(variant=v)
+        od = O.convection("deep", s, T, q, oo)
+        both_close(deep, od)
+        both_close(sh, O.convection("shallow", s, T, q, oo))
+        if v == 2:
+            assert np.array_equal(deep.work_units, od.work)
+
+
+def test_strided_rows_and_host_ld(ctx):
+    """ld > n on input and output (a column block inside a wider grid)."""
+    s, T, q = G.make_config("c1", n=1000, seed=4)
+    n, L = 900, T.shape[0]
+    lib = P.load_library()
+    cols = P._Columns(n, L, 0, T.shape[1], s.ctypes.data, T.ctypes.data, q.ctypes.data, 0)
+    out = P.ColumnOutputs(np.zeros((L, 1000)), np.zeros((L, 1000)), np.zeros(n), np.zeros(n, np.int64),
+                          np.zeros(n, np.uint8))
+    st = P.Stats()
+    o = P._Outputs(out.tend_T.ctypes.data, out.tend_q.ctypes.data, out.precip.ctypes.data,
+                   out.work_units.ctypes.data, out.exited_early.ctypes.data, 1000, 0)
+    rc = lib.cvg_deep_convection(ctx._h, C.byref(cols), C.byref(P.KernelOptions()), C.byref(o), C.byref(st))
+    assert rc == 0
+    od = O.convection("deep", s[:n], np.ascontiguousarray(T[:, :n]), np.ascontiguousarray(q[:, :n]))
+    got = P.ColumnOutputs(out.tend_T[:, :n], out.tend_q[:, :n], out.precip, out.work_units, out.exited_early)
+    both_close(got, od)
+    assert not out.tend_T[:, n:].any()   # untouched padding
+
+
+def test_invalid_arguments(ctx):
+    lib = P.load_library()
+    s, T, q = G.make_config("ref", n=64, seed=1)
+    cols = P._Columns(64, 30, 0, 32, s.ctypes.data, T.ctypes.data, q.ctypes.data, 0)  # ld < n
+    assert lib.cvg_convect(ctx._h, C.byref(cols), C.byref(P.KernelOptions()), 3, None, None, None) == 1
+    cols = P._Columns(64, 0, 0, 64, s.ctypes.data, T.ctypes.data, q.ctypes.data, 0)   # L = 0
+    assert lib.cvg_convect(ctx._h, C.byref(cols), C.byref(P.KernelOptions()), 3, None, None, None) == 1
+    assert lib.cvg_last_error()
+    with pytest.raises(ValueError):
+        ctx.convect(s, T, q, P.KernelOptions(variant=5))
+
+
+def test_device_resident_async_path(ctx):
+    import torch
+    s, T, q = G.make_config("c2", seed=9)
+    dev = torch.device("cuda", 0)
+    ds, dT, dq = (torch.from_numpy(a).to(dev) for a in (s, T, q))
+    L, n = T.shape
+
+    def outs():
+        return (torch.empty((L, n), dtype=torch.float64, device=dev), torch.empty((L, n), dtype=torch.float64, device=dev),
+                torch.empty(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.int64, device=dev),
+                torch.empty(n, dtype=torch.uint8, device=dev))
+    do, so = outs(), outs()
+    stream = torch.cuda.Stream()
+    ctx.convect_async(ds, dT, dq, do, so, stream=stream)
+    st = ctx.check(stream)
+    assert st.n_triggered == int((s > 0.5).sum())
+    got = P.ColumnOutputs(*[t.cpu().numpy() for t in do])
+    both_close(got, O.convection("deep", s, T, q))
+    # latched device error surfaces at check()
+    ds[7] = float("nan")
+    ctx.convect_async(ds, dT, dq, do, so, stream=stream)
+    with pytest.raises(P.KernelError) as e:
+        ctx.check(stream)
+    assert e.value.column == 7
