@@ -55,9 +55,22 @@ def build_oracle(force=False):
     _run(args)
 
 
+def build_cpp_tests(force=False):
+    """tests/cpp/test_dropin: the C++ drop-in vs the reference's own types and
+    CPU implementation (needs the reference headers: build container only)."""
+    ref_src = os.environ.get("CONVPROXY_REF", "/root/reference/proj/src/core")
+    if not os.path.isdir(ref_src):
+        return
+    args = ["make", "-C", os.path.join(ROOT, "tests", "cpp"), f"REF={ref_src}"]
+    if force:
+        args.insert(1, "-B")
+    _run(args)
+
+
 def build_all(force=False):
     build_cuda(force)
     build_oracle(force)
+    build_cpp_tests(force)
 
 
 if __name__ == "__main__":
