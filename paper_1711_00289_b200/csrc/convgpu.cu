@@ -116,6 +116,8 @@ struct cvg_context {
   DevBuf<int> auxi;
   int col_warps = 8;                   // column-stream warps per fused block
   bool fused = false;                  // fused persistent kernel vs split kernels
+  bool overlap = true;                 // split kernels on two streams, concurrently
+  cudaStream_t main_for_join = nullptr;
   int shallow_mode = 0;                // 0 plain, 1 L2-prefetched stream, 2 TMA-staged
   // per-kernel profiling (cvg_profile_begin/end)
   bool prof_on = false;
@@ -169,12 +171,12 @@ void launch_fused_t(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::Shallow
   CVG_CUDA(cudaGetLastError());
 }
 
-template <int VAR, bool NARROW>
+template <int VAR, bool NARROW, int NW>
 void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
-  const int threads = cvg::kFusedWarps * 32;
+  const int threads = NW * 32;
   const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
-                      (size_t)cvg::kFusedWarps * a.batch * a.L * sizeof(double);
-  auto kern = cvg::deep_kernel<VAR, NARROW>;
+                      (size_t)NW * a.batch * a.L * sizeof(double);
+  auto kern = cvg::deep_kernel<VAR, NARROW, NW>;
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<ctx->num_sms, threads, smem, st>>>(a);
   CVG_CUDA(cudaGetLastError());
@@ -183,11 +185,25 @@ void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
 template <int VAR>
 void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh, bool dp,
                   cudaEvent_t* pe, cudaStream_t st) {
+  // overlap: the FP64-bound deep kernel (one 20-warp block per SM, launched
+  // first) and the HBM-bound shallow kernel (forked onto the side stream,
+  // its blocks fill the rest of each SM) run concurrently
+  const bool ov = ctx->overlap && dp;
+  if (ov) CVG_CUDA(cudaEventRecord(ctx->ev_fork, st));
   if (dp) {
-    if (a.L <= 32) launch_deep_t<VAR, true>(ctx, a, st);
-    else launch_deep_t<VAR, false>(ctx, a, st);
+    if (ov) {
+      if (a.L <= 32) launch_deep_t<VAR, true, cvg::kDeepWarpsOverlap>(ctx, a, st);
+      else launch_deep_t<VAR, false, cvg::kDeepWarpsOverlap>(ctx, a, st);
+    } else {
+      if (a.L <= 32) launch_deep_t<VAR, true, cvg::kFusedWarps>(ctx, a, st);
+      else launch_deep_t<VAR, false, cvg::kFusedWarps>(ctx, a, st);
+    }
   }
   if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
+  if (ov) {
+    CVG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    st = ctx->side;
+  }
   if (ctx->shallow_mode == 1) {
     int occ = 0;
     auto k = sh && dp ? cvg::shallow_stream_kernel<VAR, true, true>
@@ -209,6 +225,11 @@ void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowAr
     else if (dp) cvg::shallow_kernel<VAR, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
   }
   CVG_CUDA(cudaGetLastError());
+  if (ov) {
+    if (pe) CVG_CUDA(cudaEventRecord(pe[3], st));
+    CVG_CUDA(cudaEventRecord(ctx->ev_join, st));
+    CVG_CUDA(cudaStreamWaitEvent(ctx->main_for_join, ctx->ev_join, 0));
+  }
 }
 
 template <int VAR>
@@ -275,6 +296,7 @@ void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int 
   b.err = ctx->err.p + 1; b.exp_tab = ctx->exp_tab.p; b.first_col = in->first_col;
   b.thr = o->activity_threshold; b.L = L;
   const int ncw = std::min(cvg::kFusedWarps, std::max(1, ctx->col_warps));
+  ctx->main_for_join = st;
   if (ctx->fused) {
     switch (o->variant) {
       case 1: launch_fused<cvg::kVarReduced>(ctx, a, b, do_sh, do_deep, ncw, st); break;
@@ -289,7 +311,7 @@ void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int 
       default: launch_split<cvg::kVarExact>(ctx, a, b, do_sh, do_deep, pe, st); break;
     }
   }
-  if (pe) CVG_CUDA(cudaEventRecord(pe[3], st));
+  if (pe && !(ctx->overlap && do_deep && !ctx->fused)) CVG_CUDA(cudaEventRecord(pe[3], st));
 }
 
 // Reads back the latched failure words (stream already synchronised).
@@ -416,6 +438,7 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
       // probe that the sm_100a image loads on this device
       if (const char* e = getenv("CVG_COL_WARPS")) ctx->col_warps = atoi(e);
       if (const char* e = getenv("CVG_FUSED")) ctx->fused = atoi(e) != 0;
+      if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
       if (const char* e = getenv("CVG_SHALLOW_MODE")) ctx->shallow_mode = atoi(e);
     } catch (...) {
       cvg_context_free(ctx);

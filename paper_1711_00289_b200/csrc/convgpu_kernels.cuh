@@ -704,14 +704,15 @@ __global__ void __launch_bounds__(kShTile, 1) shallow_tma_kernel(ShallowArgs a) 
 // exp table replicated kTabCopies times (bank-conflict-free lookups) and
 // each warp's deep precip batch.
 constexpr int kFusedWarps = 24;
+constexpr int kDeepWarpsOverlap = 20;  // leaves an SM's worth of room for shallow blocks
 
 // Standalone deep kernel (split mode): every warp of the persistent block
 // works the deep list.
-template <int VAR, bool NARROW>
-__global__ void __launch_bounds__(kFusedWarps * 32, 1) deep_kernel(DeepArgs a) {
+template <int VAR, bool NARROW, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) deep_kernel(DeepArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ int s_bcol[kFusedWarps][kDeepBatch];
-  __shared__ int s_bwork[kFusedWarps][kDeepBatch];
+  __shared__ int s_bcol[NW][kDeepBatch];
+  __shared__ int s_bwork[NW][kDeepBatch];
   double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
   if (VAR != kVarApprox) {
     for (int i = threadIdx.x; i < kExpTableSize * kTabCopies; i += blockDim.x)
