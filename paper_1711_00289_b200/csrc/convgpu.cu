@@ -114,11 +114,12 @@ struct cvg_context {
   DevBuf<uint8_t> dx, sx;
   DevBuf<double> aux0, aux1;
   DevBuf<int> auxi;
-  int col_warps = 8;                   // column-stream warps per fused block
-  bool fused = false;                  // fused persistent kernel vs split kernels
   bool overlap = true;                 // split kernels on two streams, concurrently
+  int shallow_minb = 8;                // shallow kernel min blocks/SM (register cap)
+  const char* trace_path = nullptr;    // CVG_TRACE: dump per-block (kernel, smid, start, end)
+  DevBuf<unsigned long long> trace_d, trace_s;
   cudaStream_t main_for_join = nullptr;
-  int shallow_mode = 0;                // 0 plain, 1 L2-prefetched stream, 2 TMA-staged
+  int shallow_mode = 0;                // 0 plain (thread per column), 2 TMA-staged tiles
   // per-kernel profiling (cvg_profile_begin/end)
   bool prof_on = false;
   int prof_cap = 0, prof_n = 0;
@@ -156,21 +157,6 @@ bool valid_options(const cvg_options* o, std::string* why) {
   return true;
 }
 
-// Launch of the fused persistent kernel (cvg::convect_kernel): one block per
-// SM; n_col_warps of its warps stream the shallow scheme + deep zero-fill
-// while the rest work the compacted deep list.
-template <int VAR, bool NARROW, bool SH, bool DP>
-void launch_fused_t(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, int n_col_warps,
-                    cudaStream_t st) {
-  const int threads = cvg::kFusedWarps * 32;
-  const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
-                      (DP ? (size_t)cvg::kFusedWarps * a.batch * a.L * sizeof(double) : 0);
-  auto kern = cvg::convect_kernel<VAR, NARROW, SH, DP>;
-  CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<ctx->num_sms, threads, smem, st>>>(a, b, n_col_warps, ctx->cursor.p + 40);
-  CVG_CUDA(cudaGetLastError());
-}
-
 template <int VAR, bool NARROW, int NW>
 void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
   const int threads = NW * 32;
@@ -178,6 +164,8 @@ void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
                       (size_t)NW * a.batch * a.L * sizeof(double);
   auto kern = cvg::deep_kernel<VAR, NARROW, NW>;
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // full shared-memory carveout, so a shallow block still fits beside it
+  CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   kern<<<ctx->num_sms, threads, smem, st>>>(a);
   CVG_CUDA(cudaGetLastError());
 }
@@ -195,8 +183,8 @@ void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowAr
       if (a.L <= 32) launch_deep_t<VAR, true, cvg::kDeepWarpsOverlap>(ctx, a, st);
       else launch_deep_t<VAR, false, cvg::kDeepWarpsOverlap>(ctx, a, st);
     } else {
-      if (a.L <= 32) launch_deep_t<VAR, true, cvg::kFusedWarps>(ctx, a, st);
-      else launch_deep_t<VAR, false, cvg::kFusedWarps>(ctx, a, st);
+      if (a.L <= 32) launch_deep_t<VAR, true, cvg::kDeepWarps>(ctx, a, st);
+      else launch_deep_t<VAR, false, cvg::kDeepWarps>(ctx, a, st);
     }
   }
   if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
@@ -204,14 +192,7 @@ void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowAr
     CVG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     st = ctx->side;
   }
-  if (ctx->shallow_mode == 1) {
-    int occ = 0;
-    auto k = sh && dp ? cvg::shallow_stream_kernel<VAR, true, true>
-                      : sh ? cvg::shallow_stream_kernel<VAR, true, false>
-                           : cvg::shallow_stream_kernel<VAR, false, true>;
-    CVG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, 0));
-    k<<<ctx->num_sms * std::max(occ, 1), 128, 0, st>>>(b);
-  } else if (ctx->shallow_mode == 2 && (b.ld_in % 2) == 0) {
+  if (ctx->shallow_mode == 2 && (b.ld_in % 2) == 0) {
     const size_t smem = (size_t)cvg::kExpTableSize * sizeof(double2) +
                         (size_t)2 * 2 * b.L * cvg::kShTile * sizeof(double);
     auto k = sh && dp ? cvg::shallow_tma_kernel<VAR, true, true>
@@ -220,7 +201,10 @@ void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowAr
     k<<<ctx->num_sms, cvg::kShTile, smem, st>>>(b);
   } else {
     const unsigned blocks = (unsigned)((b.n + cvg::kShallowThreads - 1) / cvg::kShallowThreads);
-    if (sh && dp) cvg::shallow_kernel<VAR, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    CVG_CUDA(cudaFuncSetAttribute(cvg::shallow_kernel<VAR, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    if (ctx->shallow_minb == 10 && sh && dp)
+      cvg::shallow_kernel<VAR, true, true, 10><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    else if (sh && dp) cvg::shallow_kernel<VAR, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
     else if (sh) cvg::shallow_kernel<VAR, true, false><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
     else if (dp) cvg::shallow_kernel<VAR, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
   }
@@ -232,31 +216,16 @@ void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowAr
   }
 }
 
-template <int VAR>
-void launch_fused(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh, bool dp,
-                  int n_col_warps, cudaStream_t st) {
-  const bool narrow = a.L <= 32;
-  if (sh && dp) {
-    if (narrow) launch_fused_t<VAR, true, true, true>(ctx, a, b, n_col_warps, st);
-    else launch_fused_t<VAR, false, true, true>(ctx, a, b, n_col_warps, st);
-  } else if (dp) {
-    if (narrow) launch_fused_t<VAR, true, false, true>(ctx, a, b, n_col_warps, st);
-    else launch_fused_t<VAR, false, false, true>(ctx, a, b, n_col_warps, st);
-  } else {
-    launch_fused_t<VAR, true, true, false>(ctx, a, b, cvg::kFusedWarps, st);
-  }
-}
-
 // Enqueues the hot path on `st`: memsets of the per-call cursors and
 // failure words, the trigger + compaction kernel (deep requested), then the
-// fused persistent kernel.  Pointers are device pointers.
+// deep kernel and the shallow(+zero-fill) kernel -- concurrently on a forked
+// side stream in overlap mode (the default).  Pointers are device pointers.
 void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int mask,
              const cvg_outputs* deep, const cvg_outputs* sh, cudaStream_t st) {
   const long long n = in->n_columns;
   const int L = in->n_levels;
   CVG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(int), st));
   CVG_CUDA(cudaMemsetAsync(ctx->cursor.p, 0, sizeof(unsigned long long), st));
-  CVG_CUDA(cudaMemsetAsync(ctx->cursor.p + 40, 0, sizeof(unsigned long long), st));
   CVG_CUDA(cudaMemsetAsync(ctx->err.p, 0xff, 2 * sizeof(unsigned long long), st));
   if (n == 0) return;
   const bool do_deep = (mask & CVG_DEEP) != 0, do_sh = (mask & CVG_SHALLOW) != 0;
@@ -278,7 +247,7 @@ void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int 
     a.err = ctx->err.p; a.first_col = in->first_col;
     a.thr = o->activity_threshold; a.tol = o->newton_tol; a.maxit = o->newton_max_iter;
     a.L = L;
-    a.batch = std::max(1, std::min(cvg::kDeepBatch, (int)(98304 / ((size_t)cvg::kFusedWarps * L * sizeof(double)))));
+    a.batch = std::max(1, std::min(cvg::kDeepBatch, (int)(98304 / ((size_t)cvg::kDeepWarps * L * sizeof(double)))));
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
   }
   a.exp_tab = ctx->exp_tab.p;
@@ -295,23 +264,21 @@ void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int 
   }
   b.err = ctx->err.p + 1; b.exp_tab = ctx->exp_tab.p; b.first_col = in->first_col;
   b.thr = o->activity_threshold; b.L = L;
-  const int ncw = std::min(cvg::kFusedWarps, std::max(1, ctx->col_warps));
-  ctx->main_for_join = st;
-  if (ctx->fused) {
-    switch (o->variant) {
-      case 1: launch_fused<cvg::kVarReduced>(ctx, a, b, do_sh, do_deep, ncw, st); break;
-      case 2: launch_fused<cvg::kVarApprox>(ctx, a, b, do_sh, do_deep, ncw, st); break;
-      default: launch_fused<cvg::kVarExact>(ctx, a, b, do_sh, do_deep, ncw, st); break;
-    }
-    if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
-  } else {
-    switch (o->variant) {
-      case 1: launch_split<cvg::kVarReduced>(ctx, a, b, do_sh, do_deep, pe, st); break;
-      case 2: launch_split<cvg::kVarApprox>(ctx, a, b, do_sh, do_deep, pe, st); break;
-      default: launch_split<cvg::kVarExact>(ctx, a, b, do_sh, do_deep, pe, st); break;
-    }
+  if (ctx->trace_path) {
+    ctx->trace_d.ensure(3 * 4096);
+    ctx->trace_s.ensure(3 * (size_t)((n + 127) / 128 + 1));
+    CVG_CUDA(cudaMemsetAsync(ctx->trace_d.p, 0, 3 * 4096 * 8, st));
+    CVG_CUDA(cudaMemsetAsync(ctx->trace_s.p, 0, 3 * ((n + 127) / 128 + 1) * 8, st));
+    a.trace = ctx->trace_d.p;
+    b.trace = ctx->trace_s.p;
   }
-  if (pe && !(ctx->overlap && do_deep && !ctx->fused)) CVG_CUDA(cudaEventRecord(pe[3], st));
+  ctx->main_for_join = st;
+  switch (o->variant) {
+    case 1: launch_split<cvg::kVarReduced>(ctx, a, b, do_sh, do_deep, pe, st); break;
+    case 2: launch_split<cvg::kVarApprox>(ctx, a, b, do_sh, do_deep, pe, st); break;
+    default: launch_split<cvg::kVarExact>(ctx, a, b, do_sh, do_deep, pe, st); break;
+  }
+  if (pe && !(ctx->overlap && do_deep)) CVG_CUDA(cudaEventRecord(pe[3], st));
 }
 
 // Reads back the latched failure words (stream already synchronised).
@@ -436,9 +403,9 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
       CVG_CUDA(cudaMemset(ctx->counters.p, 0, 4 * sizeof(int)));
       CVG_CUDA(cudaMemset(ctx->err.p, 0xff, 4 * sizeof(unsigned long long)));
       // probe that the sm_100a image loads on this device
-      if (const char* e = getenv("CVG_COL_WARPS")) ctx->col_warps = atoi(e);
-      if (const char* e = getenv("CVG_FUSED")) ctx->fused = atoi(e) != 0;
       if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
+      if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
+      ctx->trace_path = getenv("CVG_TRACE");
       if (const char* e = getenv("CVG_SHALLOW_MODE")) ctx->shallow_mode = atoi(e);
     } catch (...) {
       cvg_context_free(ctx);
@@ -510,6 +477,19 @@ cvg_status cvg_convect_check(cvg_context* ctx, void* stream, cvg_stats* stats) {
     CVG_CUDA(cudaStreamSynchronize(st));
     if (stats) std::memset(stats, 0, sizeof(*stats));
     if (!ctx->pending) return CVG_OK;
+    if (ctx->trace_path && ctx->trace_d.p) {
+      const size_t nd = 3 * 4096, ns = 3 * (size_t)((ctx->last_n + 127) / 128 + 1);
+      std::vector<unsigned long long> hd(nd), hs(ns);
+      CVG_CUDA(cudaMemcpy(hd.data(), ctx->trace_d.p, nd * 8, cudaMemcpyDeviceToHost));
+      CVG_CUDA(cudaMemcpy(hs.data(), ctx->trace_s.p, ns * 8, cudaMemcpyDeviceToHost));
+      if (FILE* f = fopen(ctx->trace_path, "w")) {
+        for (size_t i = 0; i + 2 < nd; i += 3)
+          if (hd[i + 1]) fprintf(f, "deep %llu %llu %llu\n", hd[i], hd[i + 1], hd[i + 2]);
+        for (size_t i = 0; i + 2 < ns; i += 3)
+          if (hs[i + 1]) fprintf(f, "shallow %llu %llu %llu\n", hs[i], hs[i + 1], hs[i + 2]);
+        fclose(f);
+      }
+    }
     return collect(ctx, ctx->last_mask, ctx->last_maxit, ctx->last_n, stats);
   });
 }

@@ -12,8 +12,8 @@
 //                           cyclically with the next column prefetched;
 //                           ordered precip sum per column inside the warp
 //   shallow_kernel          shallow scheme (physics.cpp:168-225), one thread
-//                           per column, streaming level-major rows, fused with
-//                           the zero-fill of untriggered deep columns
+//                           per column, streaming level-major rows, together
+//                           with the zero-fill of untriggered deep columns
 //                           (physics.cpp:89-97, :111-113)
 //   ientropy_kernel         batched ientropy_solve (physics.cpp:101-104)
 //   approx_exp_kernel       approx_exp (physics.cpp:40-60)
@@ -139,6 +139,7 @@ struct DeepArgs {
   uint8_t* exited;
   long long ld_out;
   const int* idx;         // compacted triggered columns
+  unsigned long long* trace;  // optional [grid][3]: smid, start, end (globaltimer ns)
   const int* count;       // number of triggered columns (device)
   unsigned long long* cursor;  // [0] work cursor (zeroed per call), [1..32] dummies
   unsigned long long* err;
@@ -447,7 +448,19 @@ struct ShallowArgs {
   long long first_col;
   double thr;
   int L;
+  unsigned long long* trace;  // optional [grid][3]: smid, start, end (globaltimer ns)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 // One column of the shallow scheme (and/or the deep zero-fill), one thread.
 // STRIDE: exp table layout (1 = plain, kTabCopies = replicated, lane copy).
@@ -580,52 +593,22 @@ __device__ __forceinline__ void shallow_column(const ShallowArgs& a, long long c
 constexpr int kShallowThreads = 128;
 
 // Standalone shallow(+zero-fill) kernel: one thread per column.
-template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO>
-__global__ void __launch_bounds__(kShallowThreads, 8) shallow_kernel(ShallowArgs a) {
+template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO, int MINB = 8>
+__global__ void __launch_bounds__(kShallowThreads, MINB) shallow_kernel(ShallowArgs a) {
   __shared__ double2 s_tab[kExpTableSize];
   if (DO_SHALLOW && VAR != kVarApprox) {
     for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
     __syncthreads();
   }
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= a.n) return;
-  shallow_column<VAR, DO_SHALLOW, DO_DEEP_ZERO, 1>(a, c, s_tab);
-}
-
-// ---------------------------------------------------------------------------
-// Streaming shallow(+zero-fill) kernel, L2-prefetched: persistent blocks of
-// kShTile threads walk tiles of kShTile columns (a thread per column,
-// registers-only, 8 blocks per SM); while a block computes tile t, one lane
-// asks the TMA engine to prefetch tile t + G's 2 L rows into L2, so the
-// per-thread row loads of the next tile are L2 hits instead of HBM round
-// trips.  No shared-memory staging: occupancy stays at 32 warps/SM for the
-// per-column serial chains (the ordered level sums, physics.cpp:183-204).
-template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO>
-__global__ void __launch_bounds__(128, 8) shallow_stream_kernel(ShallowArgs a) {
-  __shared__ double2 s_tab[kExpTableSize];
-  if (DO_SHALLOW && VAR != kVarApprox) {
-    for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
+  if (a.trace && threadIdx.x == 0) {
+    a.trace[3 * blockIdx.x] = smid();
+    a.trace[3 * blockIdx.x + 1] = gtimer();
   }
-  __syncthreads();
-  const int L = a.L;
-  const long long ntiles = (a.n + 127) / 128;
-  auto prefetch = [&](long long tile) {
-    const long long c0 = tile * 128;
-    const long long cols = min(128LL, a.n - c0);
-    const unsigned bytes = (unsigned)(((cols * 8) + 15) & ~15LL);
-    const bool ok = ((a.ld_in & 1) == 0) && (c0 + (bytes / 8) <= a.ld_in);
-    if (!ok) return;
-    for (int k = (int)threadIdx.x; k < 2 * L; k += blockDim.x) {
-      const double* base = (k < L ? a.T + (long long)k * a.ld_in : a.q + (long long)(k - L) * a.ld_in) + c0;
-      bulk_prefetch_l2(base, bytes);
-    }
-  };
-  long long tile = blockIdx.x;
-  if (DO_SHALLOW && tile < ntiles) prefetch(tile);
-  for (; tile < ntiles; tile += gridDim.x) {
-    if (DO_SHALLOW && tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
-    const long long c = tile * 128 + threadIdx.x;
-    if (c < a.n) shallow_column<VAR, DO_SHALLOW, DO_DEEP_ZERO, 1>(a, c, s_tab);
+  if (c < a.n) shallow_column<VAR, DO_SHALLOW, DO_DEEP_ZERO, 1>(a, c, s_tab);
+  if (a.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.trace[3 * blockIdx.x + 2] = gtimer();
   }
 }
 
@@ -694,23 +677,19 @@ __global__ void __launch_bounds__(kShTile, 1) shallow_tma_kernel(ShallowArgs a) 
 }
 
 // ---------------------------------------------------------------------------
-// Fused persistent convection kernel: one block per SM, kFusedWarps warps.
-// The deep plume is FP64-bound and the shallow scheme + deep zero-fill
-// HBM-bound, so one kernel runs both at once by warp specialisation:
-// warps [0, n_col_warps) first stream column tiles (32 columns, a thread
-// per column) for the shallow scheme and the zero-fill, claiming tiles from
-// a global cursor; the remaining warps -- and the column warps once the
-// tiles run out -- work the deep list.  The block's shared memory holds the
-// exp table replicated kTabCopies times (bank-conflict-free lookups) and
-// each warp's deep precip batch.
-constexpr int kFusedWarps = 24;
+// Persistent deep kernel: one block per SM; every warp works the deep list
+// (deep_worker).  kDeepWarps when it runs alone, kDeepWarpsOverlap when the
+// shallow kernel shares the SMs (convgpu.cu, overlap mode).
+constexpr int kDeepWarps = 24;
 constexpr int kDeepWarpsOverlap = 20;  // leaves an SM's worth of room for shallow blocks
 
-// Standalone deep kernel (split mode): every warp of the persistent block
-// works the deep list.
 template <int VAR, bool NARROW, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) deep_kernel(DeepArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  if (a.trace && threadIdx.x == 0) {
+    a.trace[3 * blockIdx.x] = smid();
+    a.trace[3 * blockIdx.x + 1] = gtimer();
+  }
   __shared__ int s_bcol[NW][kDeepBatch];
   __shared__ int s_bwork[NW][kDeepBatch];
   double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
@@ -724,45 +703,9 @@ __global__ void __launch_bounds__(NW * 32, 1) deep_kernel(DeepArgs a) {
   double* s_term = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies) +
                    (size_t)wib * a.batch * a.L;
   deep_worker<VAR, NARROW>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], lane);
-}
-
-template <int VAR, bool NARROW, bool DO_SH, bool DO_DEEP>
-__global__ void __launch_bounds__(kFusedWarps * 32, 1)
-convect_kernel(DeepArgs a, ShallowArgs b, int n_col_warps, unsigned long long* tile_cursor) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ int s_bcol[kFusedWarps][kDeepBatch];
-  __shared__ int s_bwork[kFusedWarps][kDeepBatch];
-  double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
-  if (VAR != kVarApprox) {
-    for (int i = threadIdx.x; i < kExpTableSize * kTabCopies; i += blockDim.x)
-      s_tab_all[i] = a.exp_tab[i / kTabCopies];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const double2* s_tab = s_tab_all + (lane & (kTabCopies - 1));
-  if ((DO_SH || DO_DEEP) && wib < n_col_warps) {
-    // column-stream role; the next tile is claimed a tile ahead (every lane
-    // issues the atomic so it is not warp-aggregated, see deep_worker)
-    const long long ntiles = (b.n + 31) / 32;
-    long long next_raw = 0;
-    auto claim = [&]() {
-      unsigned long long* addr = lane == 0 ? tile_cursor : tile_cursor + 1 + lane;
-      next_raw = (long long)atomicAdd(addr, lane == 0 ? 1ULL : 0ULL);
-    };
-    claim();
-    long long tile = __shfl_sync(0xffffffffu, next_raw, 0);
-    claim();
-    while (tile < ntiles) {
-      const long long c = tile * 32 + lane;
-      if (c < b.n) shallow_column<VAR, DO_SH, DO_DEEP, kTabCopies>(b, c, s_tab);
-      tile = __shfl_sync(0xffffffffu, next_raw, 0);
-      claim();
-    }
-  }
-  if (DO_DEEP) {
-    double* s_term = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies) +
-                     (size_t)wib * a.batch * a.L;
-    deep_worker<VAR, NARROW>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], lane);
+  if (a.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.trace[3 * blockIdx.x + 2] = gtimer();
   }
 }
 
