@@ -120,6 +120,8 @@ struct cvg_context {
   DevBuf<unsigned long long> trace_d, trace_s;
   cudaStream_t main_for_join = nullptr;
   int shallow_mode = 0;                // 0 plain (thread per column), 2 TMA-staged tiles
+  bool pairs = false;                  // deep: two columns per warp (ILP 4)
+  int shallow_persist = 0;             // overlap: persistent shallow blocks per SM (0 = grid of tiles)
   // per-kernel profiling (cvg_profile_begin/end)
   bool prof_on = false;
   int prof_cap = 0, prof_n = 0;
@@ -157,12 +159,12 @@ bool valid_options(const cvg_options* o, std::string* why) {
   return true;
 }
 
-template <int VAR, bool NARROW, int NW>
+template <int VAR, bool NARROW, int NW, bool PAIRS = false>
 void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
   const int threads = NW * 32;
   const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
                       (size_t)NW * a.batch * a.L * sizeof(double);
-  auto kern = cvg::deep_kernel<VAR, NARROW, NW>;
+  auto kern = cvg::deep_kernel<VAR, NARROW, NW, PAIRS>;
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // full shared-memory carveout, so a shallow block still fits beside it
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -179,7 +181,10 @@ void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowAr
   const bool ov = ctx->overlap && dp;
   if (ov) CVG_CUDA(cudaEventRecord(ctx->ev_fork, st));
   if (dp) {
-    if (ov) {
+    if (ctx->pairs && a.L <= 32) {
+      if (ov) launch_deep_t<VAR, true, 14, true>(ctx, a, st);
+      else launch_deep_t<VAR, true, 16, true>(ctx, a, st);
+    } else if (ov) {
       if (a.L <= 32) launch_deep_t<VAR, true, cvg::kDeepWarpsOverlap>(ctx, a, st);
       else launch_deep_t<VAR, false, cvg::kDeepWarpsOverlap>(ctx, a, st);
     } else {
@@ -192,7 +197,13 @@ void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowAr
     CVG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     st = ctx->side;
   }
-  if (ctx->shallow_mode == 2 && (b.ld_in % 2) == 0) {
+  if (ov && ctx->shallow_persist > 0) {
+    auto k = sh && dp ? cvg::shallow_persistent_kernel<VAR, true, true>
+                      : sh ? cvg::shallow_persistent_kernel<VAR, true, false>
+                           : cvg::shallow_persistent_kernel<VAR, false, true>;
+    CVG_CUDA(cudaMemsetAsync(ctx->cursor.p + 40, 0, sizeof(unsigned long long), st));
+    k<<<ctx->num_sms * ctx->shallow_persist, cvg::kShallowThreads, 0, st>>>(b, ctx->cursor.p + 40);
+  } else if (ctx->shallow_mode == 2 && (b.ld_in % 2) == 0) {
     const size_t smem = (size_t)cvg::kExpTableSize * sizeof(double2) +
                         (size_t)2 * 2 * b.L * cvg::kShTile * sizeof(double);
     auto k = sh && dp ? cvg::shallow_tma_kernel<VAR, true, true>
@@ -407,6 +418,8 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
       if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
       ctx->trace_path = getenv("CVG_TRACE");
       if (const char* e = getenv("CVG_SHALLOW_MODE")) ctx->shallow_mode = atoi(e);
+      if (const char* e = getenv("CVG_PAIRS")) ctx->pairs = atoi(e) != 0;
+      if (const char* e = getenv("CVG_SHALLOW_PERSIST")) ctx->shallow_persist = atoi(e);
     } catch (...) {
       cvg_context_free(ctx);
       throw;

@@ -418,6 +418,258 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
 }
 
 // ---------------------------------------------------------------------------
+// Lockstep Newton over NS independent solves of one lane (physics.cpp:
+// 64-87 each).  Every iteration tests each solve and records its FIRST
+// convergence (root, update count); all NS solves are then updated
+// unconditionally -- a converged solve keeps taking (harmless, in-domain)
+// Newton steps whose results are never used -- so the loop body is
+// straight-line FP64 with NS independent dependency chains.  Solves whose
+// fast-path precondition failed (see deep_lane_pair) enter with their bit
+// set in `done` and are finished by the caller with newton_generic, as are
+// solves still unconverged after max_iter updates.
+template <int VAR, int NS>
+__device__ __forceinline__ void newton_lockstep(const double2* tab, double tol, int maxit, double* t,
+                                                double* e, double* h, const double* y, double* root,
+                                                int* cnt, unsigned& done) {
+  const unsigned all = (1u << NS) - 1u;
+  int it = 0;
+  for (;;) {
+    // convergence bits of all solves (integer compares, no FP64 pipe); the
+    // record branch is taken about once per solve
+    unsigned conv = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) conv |= (unsigned)abs_le(h[s], tol) << s;
+    const unsigned fresh = conv & ~done;
+    if (fresh) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (fresh & (1u << s)) {
+          root[s] = t[s];
+          cnt[s] = it;
+        }
+      }
+      done |= fresh;
+    }
+    if (done == all || it >= maxit) break;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) t[s] = sub(t[s], div_fast(h[s], add(mul(kMC.c005, e[s]), kMC.c001)));
+#pragma unroll
+    for (int s = 0; s < NS; ++s) e[s] = deep_exp005_fast<VAR>(t[s], tab);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) h[s] = sub(add(e[s], mul(kMC.c001, t[s])), y[s]);
+    ++it;
+  }
+  // unconverged solves leave with their state after `it` updates
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (!(done & (1u << s))) cnt[s] = it;
+}
+
+// Per-lane state of one (column, level): inputs, the two solves' results.
+struct LevelSolve {
+  double T, q, ye, yp, re, rp;
+  int work;
+  bool ok;
+};
+
+// Two columns per warp: lane k owns level k of column A and of column B,
+// i.e. FOUR solves in lockstep (entrainment and precipitation of both).
+// Consecutive list entries sit in the same s-bucket, so the two columns'
+// iteration counts agree to within about one update; the per-warp overheads
+// (claims, reductions, batch flushes) are paid once per pair.  L <= 32.
+template <int VAR>
+__device__ __forceinline__ void deep_pair_solve(const DeepArgs& a, const double2* tab, int lane,
+                                                const long long colA, const long long colB, double sA,
+                                                double sB, LevelSolve& A, LevelSolve& B) {
+  const bool reduced = (VAR == kVarReduced);
+  const double kBig = 0x1.0p490;
+  const int k = lane;
+  double guess[2], e0[2], c0[2];
+  LevelSolve* X[2] = {&A, &B};
+  const double sv[2] = {sA, sB};
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const double sc = sv[p];
+    LevelSolve& Z = *X[p];
+    guess[p] = add(24.0, mul(160.0, sc));                       // physics.cpp:121
+    const double rho = add(1.0, mul(kMC.c005, sc));             // :127 / :146
+    e0[p] = deep_exp<VAR>(mul(kMC.c005, guess[p]), tab);
+    c0[p] = add(e0[p], mul(kMC.c001, guess[p]));
+    double m;  // physics.hpp:94-96 via the shared-divisor form of div_rn
+    const double dv = reduced ? mul(rho, rho) : rho;
+    if (div_operand_ok(dv) && div_operand_ok(Z.q)) {
+      const double ydv = rcp_refined(dv);
+      m = div_by(Z.q, dv, ydv);
+      if (!reduced) m = div_operand_ok(m) ? div_by(m, dv, ydv) : div_rn(m, dv);
+    } else {
+      m = reduced ? div_rn(Z.q, dv) : div_rn(div_rn(Z.q, rho), rho);
+    }
+    Z.ye = add(add(1.0, mul(1.0e-3, Z.T)), mul(0.1, m));                      // :147-148
+    Z.yp = add(add(add(1.0, mul(8.0e-4, Z.T)), mul(kMC.c005, m)), mul(0.1, sc));  // :156-157
+  }
+  // solve s: 0 = A.entr, 1 = A.prec, 2 = B.entr, 3 = B.prec
+  double t[4], e[4], h[4], y[4], root[4];
+  int cnt[4];
+  unsigned done = 0;
+  const bool fast_tol = a.fast_div_ok;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int p = s >> 1;
+    y[s] = (s & 1) ? X[p]->yp : X[p]->ye;
+    t[s] = guess[p];
+    e[s] = e0[p];
+    h[s] = sub(c0[p], y[s]);
+    root[s] = 0.0;
+    cnt[s] = 0;
+    const bool fast = fast_tol && is_finite(y[s]) && y[s] > -60.0 && y[s] < kBig && h[s] > 0.0 &&
+                      exp_fast_ok(mul(kMC.c005, guess[p]));
+    if (!fast) done |= 1u << s;
+  }
+  const unsigned slow = done;
+  newton_lockstep<VAR, 4>(tab, a.tol, a.maxit, t, e, h, y, root, cnt, done);
+  A.ok = B.ok = true;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int p = s >> 1;
+    LevelSolve& Z = *X[p];
+    const long long col = p ? colB : colA;
+    const int order = (s & 1) ? a.L + k : k;
+    if (!(done & (1u << s)) || (slow & (1u << s))) {
+      // slow-path or unconverged solve: reference-faithful generic loop
+      if (!is_finite(y[s])) {
+        raise_failure(a.err, col, order, kFailInput);
+        Z.ok = false;
+        continue;
+      }
+      if (!newton_generic<VAR>(a, tab, col, order, y[s], t[s], e[s], h[s], cnt[s])) {
+        Z.ok = false;
+        continue;
+      }
+      root[s] = t[s];
+    }
+    if (s & 1) Z.rp = root[s]; else Z.re = root[s];
+  }
+  A.work = cnt[0] + cnt[1];
+  B.work = cnt[2] + cnt[3];
+}
+
+// Pair worker: the warp claims chunks of kDeepChunk list entries (pairs
+// (j, j+1), j even), prefetches the next pair's (s, T[lane], q[lane]) behind
+// the current pair's solves, and finishes per-column scalars in batches.
+template <int VAR>
+__device__ __forceinline__ void deep_worker_pairs(const DeepArgs& a, const double2* s_tab, double* s_term,
+                                                  int* s_bcol, int* s_bwork, int lane) {
+  const int L = a.L;
+  const long long A = *a.count;
+  long long next_raw = 0;
+  auto claim = [&]() {
+    unsigned long long* addr = lane == 0 ? a.cursor : a.cursor + 1 + lane;
+    const unsigned long long inc = lane == 0 ? (unsigned long long)kDeepChunk : 0ULL;
+    next_raw = (long long)atomicAdd(addr, inc);
+  };
+  auto advance = [&](long long x) -> long long {   // next pair start
+    if (((x + 2) & (kDeepChunk - 1)) != 0) return x + 2;
+    const long long r = __shfl_sync(0xffffffffu, next_raw, 0);
+    claim();
+    return r;
+  };
+  claim();
+  long long j = __shfl_sync(0xffffffffu, next_raw, 0);
+  claim();
+  long long jn = advance(j);
+  auto col_of = [&](long long x) -> int { return x < A ? a.idx[x] : -1; };
+  int cA = col_of(j), cB = col_of(j + 1), nA = col_of(jn), nB = col_of(jn + 1);
+  auto ld = [&](int c, double& s, double& T, double& q) {
+    const int cc = c < 0 ? 0 : c;
+    s = a.s[cc];
+    if (lane < L) {
+      T = a.T[(long long)lane * a.ld_in + cc];
+      q = a.q[(long long)lane * a.ld_in + cc];
+    }
+  };
+  double sA = 0, TA = 0, qA = 0, sB = 0, TB = 0, qB = 0;
+  if (cA >= 0) {
+    ld(cA, sA, TA, qA);
+    ld(cB >= 0 ? cB : cA, sB, TB, qB);
+  }
+  int nb = 0;
+  while (cA >= 0) {
+    // Order matters (ptxas shares scoreboard slots between loads): first
+    // consume the values prefetched a pair ago, then issue the next pair's
+    // prefetch (its indices were loaded a pair ago), and only then the index
+    // loads for the pair after next -- so no consumer waits on a load
+    // issued in the same iteration.
+    LevelSolve XA, XB;
+    XA.T = TA; XA.q = qA;
+    XB.T = TB; XB.q = qB;
+    const double scA = sA, scB = sB;
+    const bool hasB = cB >= 0;
+    asm volatile("" ::: "memory");
+    if (nA >= 0) {  // prefetch the next pair behind the solves
+      ld(nA, sA, TA, qA);
+      ld(nB >= 0 ? nB : nA, sB, TB, qB);
+    }
+    asm volatile("" ::: "memory");
+    const long long jnn = (jn < A) ? advance(jn) : A;
+    const int mA = col_of(jnn), mB = col_of(jnn + 1);
+    XA.work = XB.work = 0;
+    XA.ok = XB.ok = true;
+    double termA = 0.0, termB = 0.0;
+    if (lane < L) {
+      deep_pair_solve<VAR>(a, s_tab, lane, a.first_col + cA, a.first_col + (hasB ? cB : cA), scA, scB, XA, XB);
+      const int k = lane;
+      // physics.cpp:151-152 / :159-161 for both columns
+      double s1, s2, s3, s4;
+      sin2_cw(add(mul(6.0, XA.T), mul(50.0, XA.q)), mul(3.0, XA.rp), s1, s2);
+      sin2_cw(add(mul(6.0, XB.T), mul(50.0, XB.q)), mul(3.0, XB.rp), s3, s4);
+      if (XA.ok) {
+        const long long o = (long long)k * a.ld_out + cA;
+        a.tend_T[o] = add(mul(0.02, sub(add(250.0, mul(2.0, XA.re)), XA.T)), mul(0.3, s1));
+        a.tend_q[o] = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, s2)), XA.q));
+        termA = mul(XA.q, max0(sub(XA.rp, 4.5)));
+      }
+      if (hasB && XB.ok) {
+        const long long o = (long long)k * a.ld_out + cB;
+        a.tend_T[o] = add(mul(0.02, sub(add(250.0, mul(2.0, XB.re)), XB.T)), mul(0.3, s3));
+        a.tend_q[o] = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, s4)), XB.q));
+        termB = mul(XB.q, max0(sub(XB.rp, 4.5)));
+      }
+      s_term[nb * L + k] = termA;
+      s_term[(nb + 1) * L + k] = termB;
+    }
+    const int wA = __reduce_add_sync(0xffffffffu, XA.work);
+    const int wB = __reduce_add_sync(0xffffffffu, XB.work);
+    const bool okA = __all_sync(0xffffffffu, XA.ok);
+    const bool okB = __all_sync(0xffffffffu, XB.ok);
+    if (lane == 0) {
+      s_bcol[nb] = okA ? cA : -1;
+      s_bwork[nb] = wA;
+      s_bcol[nb + 1] = (hasB && okB) ? cB : -1;
+      s_bwork[nb + 1] = wB;
+    }
+    nb += 2;
+    cA = nA; cB = nB; nA = mA; nB = mB;
+    jn = jnn;
+    if (nb + 2 > a.batch || cA < 0) {
+      __syncwarp();
+      if (lane < nb) {
+        const int cc = s_bcol[lane];
+        if (cc >= 0) {
+          double pr = 0.0;  // ordered k sum, physics.cpp:161
+          const double* tt = s_term + lane * L;
+          for (int kk = 0; kk < L; ++kk) pr = add(pr, tt[kk]);
+          a.precip[cc] = pr;
+          a.work[cc] = s_bwork[lane];
+          a.exited[cc] = 0;
+        }
+      }
+      __syncwarp();
+      nb = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Shallow scheme + deep zero-fill.  The four phase sums of physics.cpp:
 // 182-204 depend only on (T, q, s), not on acc, so one streaming pass over
 // the levels accumulates all four (each in k order, bit-identical to the
@@ -613,6 +865,54 @@ __global__ void __launch_bounds__(kShallowThreads, MINB) shallow_kernel(ShallowA
 }
 
 // ---------------------------------------------------------------------------
+// Persistent shallow(+zero-fill) kernel for overlap mode: NB blocks of 128
+// threads per SM share the SMs with the deep kernel's blocks.  A block walks
+// 128-column tiles (dynamic cursor, one claim per tile, issued a tile
+// ahead) and, while it computes tile t, asks the TMA engine to prefetch
+// tile t+1's 2 L rows into L2 (cp.async.bulk.prefetch), so its per-thread
+// row loads are L2 hits: the shallow work then needs little issue share to
+// keep pace with the FP64-bound deep kernel beside it.
+template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO>
+__global__ void __launch_bounds__(kShallowThreads) shallow_persistent_kernel(ShallowArgs a,
+                                                                           unsigned long long* cursor) {
+  __shared__ double2 s_tab[kExpTableSize];
+  __shared__ long long s_next;
+  if (DO_SHALLOW && VAR != kVarApprox) {
+    for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
+  }
+  const int L = a.L;
+  const long long ntiles = (a.n + kShallowThreads - 1) / kShallowThreads;
+  const bool can_prefetch = DO_SHALLOW && (a.ld_in & 1) == 0;
+  auto prefetch = [&](long long tile) {
+    if (!can_prefetch || tile >= ntiles) return;
+    const long long c0 = tile * kShallowThreads;
+    const long long cols = min((long long)kShallowThreads, a.n - c0);
+    const unsigned bytes = (unsigned)((cols * 8 + 15) & ~15LL);
+    if (c0 + bytes / 8 > a.ld_in) return;
+    for (int k = (int)threadIdx.x; k < 2 * L; k += blockDim.x) {
+      const double* base = (k < L ? a.T + (long long)k * a.ld_in : a.q + (long long)(k - L) * a.ld_in) + c0;
+      bulk_prefetch_l2(base, bytes);
+    }
+  };
+  if (threadIdx.x == 0) s_next = (long long)atomicAdd(cursor, 1ULL);
+  __syncthreads();
+  long long tile = s_next;
+  __syncthreads();
+  if (threadIdx.x == 0) s_next = (long long)atomicAdd(cursor, 1ULL);
+  prefetch(tile);
+  while (tile < ntiles) {
+    __syncthreads();
+    const long long nxt = s_next;
+    __syncthreads();
+    if (threadIdx.x == 0 && nxt < ntiles) s_next = (long long)atomicAdd(cursor, 1ULL);
+    prefetch(nxt);
+    const long long c = tile * kShallowThreads + threadIdx.x;
+    if (c < a.n) shallow_column<VAR, DO_SHALLOW, DO_DEEP_ZERO, 1>(a, c, s_tab);
+    tile = nxt;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Streaming shallow(+zero-fill) kernel on the TMA engine: one persistent
 // block per SM walks tiles of kShTile columns; thread 0 stages the next
 // tile's 2L rows (T and q, 1 KB each) into the idle half of a double buffer
@@ -683,7 +983,7 @@ __global__ void __launch_bounds__(kShTile, 1) shallow_tma_kernel(ShallowArgs a) 
 constexpr int kDeepWarps = 24;
 constexpr int kDeepWarpsOverlap = 20;  // leaves an SM's worth of room for shallow blocks
 
-template <int VAR, bool NARROW, int NW>
+template <int VAR, bool NARROW, int NW, bool PAIRS = false>
 __global__ void __launch_bounds__(NW * 32, 1) deep_kernel(DeepArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (a.trace && threadIdx.x == 0) {
@@ -702,7 +1002,8 @@ __global__ void __launch_bounds__(NW * 32, 1) deep_kernel(DeepArgs a) {
   const double2* s_tab = s_tab_all + (lane & (kTabCopies - 1));
   double* s_term = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies) +
                    (size_t)wib * a.batch * a.L;
-  deep_worker<VAR, NARROW>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], lane);
+  if (PAIRS && NARROW) deep_worker_pairs<VAR>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], lane);
+  else deep_worker<VAR, NARROW>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], lane);
   if (a.trace) {
     __syncthreads();
     if (threadIdx.x == 0) a.trace[3 * blockIdx.x + 2] = gtimer();
