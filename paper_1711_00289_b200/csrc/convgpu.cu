@@ -1,11 +1,13 @@
 // convgpu.cu -- host runtime and C ABI of the B200 convection column path.
 //
-// Implements include/convgpu.h: per-device contexts owning a persistent
-// device workspace (compaction list, cursors, latched failure words, the
-// exp table, staging buffers sized to the high-water column count), the
-// launch sequence trigger+compaction -> deep plume -> shallow(+deep zero
-// fill), host<->device staging for host buffers, the reference's error
-// taxonomy at the boundary (capi.cpp:51-89), and the multi-device partition
+// Implements include/convgpu.h: per-device contexts owning the exp table and
+// a small ring of per-call workspaces (compaction list, cursors, latched
+// failure words, a side stream for the concurrent shallow kernel, and the
+// staging buffers of host-buffer calls); the launch sequence trigger +
+// compaction -> deep plume || shallow (+ deep zero fill); host <-> device
+// staging as a chunked pipeline (H2D, compute and D2H of different column
+// chunks overlap on the copy engines and the SMs); the reference's error
+// taxonomy at the boundary (capi.cpp:51-89); and the multi-device partition
 // planner.  No CPU fallback exists: without a usable sm_100 device every
 // compute entry point returns CVG_ERR_DEVICE.
 #include <cuda_runtime.h>
@@ -91,42 +93,80 @@ const char* kind_message(int kind, int kernel, int maxit, std::string* buf) {
   }
 }
 
+// Everything one in-flight call needs on the device.  Slot 0 serves the
+// device-resident (async) API; host-buffer calls pipeline column chunks
+// through all slots.
+struct Workspace {
+  cudaStream_t stream = nullptr;  // chunk stream (host-buffer calls)
+  cudaStream_t side = nullptr;    // shallow kernel, concurrent with deep
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  DevBuf<int> idx;                     // compacted triggered columns
+  DevBuf<int> counters;                // [0] triggered count
+  DevBuf<unsigned long long> cursor;   // [0] deep work cursor, [1..32] dummies
+  DevBuf<unsigned long long> err;      // [0] deep, [1] shallow failure key
+  unsigned long long* h_err = nullptr; // pinned mirror of err[0..1]
+  int* h_count = nullptr;              // pinned mirror of counters[0]
+  // staging for host-buffer calls (chunk-sized)
+  DevBuf<double> in_s, in_T, in_q, dT, dq, dp, sT, sq, sp;
+  DevBuf<long long> dw, sw;
+  DevBuf<uint8_t> dx, sx;
+
+  void create() {
+    CVG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CVG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    CVG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CVG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    counters.ensure(4);
+    cursor.ensure(40);
+    err.ensure(4);
+    CVG_CUDA(cudaMemset(counters.p, 0, 4 * sizeof(int)));
+    CVG_CUDA(cudaMemset(cursor.p, 0, 40 * sizeof(unsigned long long)));
+    CVG_CUDA(cudaMemset(err.p, 0xff, 4 * sizeof(unsigned long long)));
+    CVG_CUDA(cudaMallocHost(&h_err, 4 * sizeof(unsigned long long)));
+    CVG_CUDA(cudaMallocHost(&h_count, 4 * sizeof(int)));
+  }
+  void destroy() {
+    for (auto* b : {&in_s, &in_T, &in_q, &dT, &dq, &dp, &sT, &sq, &sp}) b->release();
+    dw.release(); sw.release(); dx.release(); sx.release();
+    idx.release(); counters.release(); cursor.release(); err.release();
+    if (h_err) cudaFreeHost(h_err);
+    if (h_count) cudaFreeHost(h_count);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (stream) cudaStreamDestroy(stream);
+    if (side) cudaStreamDestroy(side);
+    h_err = nullptr; h_count = nullptr; ev_fork = ev_join = nullptr; stream = side = nullptr;
+  }
+};
+
+constexpr int kSlots = 4;                    // workspaces (pipeline depth of host-buffer calls)
+constexpr long long kChunkCols = 262144;     // columns per host-buffer pipeline chunk (steady state)
+
 }  // namespace
 
 struct cvg_context {
   int device = 0;
   int num_sms = 0;
-  cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;           // shallow kernel, concurrent with deep
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_h0 = nullptr, ev_h1 = nullptr, ev_d0 = nullptr;
+  cudaStream_t stream = nullptr;  // default stream of the async API
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_h0 = nullptr, ev_h1 = nullptr;
   DevBuf<double2> exp_tab;
-  DevBuf<int> idx;
-  DevBuf<int> counters;                // [0] triggered count, [2..3] deep work cursor (u64)
-  DevBuf<unsigned long long> err;      // [0] deep, [1] shallow, [2] ientropy
-  DevBuf<unsigned long long> cursor;   // deep work cursor + 32 dummy words
-  unsigned long long* h_err = nullptr; // pinned mirror
-  int* h_count = nullptr;
-  // staging for host-buffer calls
-  DevBuf<double> in_s, in_T, in_q;
-  DevBuf<double> dT, dq, dp, sT, sq, sp;
-  DevBuf<long long> dw, sw;
-  DevBuf<uint8_t> dx, sx;
+  Workspace ws[kSlots];
   DevBuf<double> aux0, aux1;
   DevBuf<int> auxi;
-  bool overlap = true;                 // split kernels on two streams, concurrently
-  int shallow_minb = 8;                // shallow kernel min blocks/SM (register cap)
-  const char* trace_path = nullptr;    // CVG_TRACE: dump per-block (kernel, smid, start, end)
+  DevBuf<unsigned long long> aux_err;
+  unsigned long long* h_aux_err = nullptr;
+  // tuning switches (environment, read at context creation)
+  bool overlap = true;     // CVG_OVERLAP: deep || shallow on two streams
+  bool pairs = false;      // CVG_PAIRS: two deep columns per warp (ILP 4)
+  int shallow_mode = 0;    // CVG_SHALLOW_MODE: 0 thread per column, 2 TMA-staged tiles
+  long long chunk_cols = kChunkCols;  // CVG_CHUNK_COLS: host-call pipeline chunk
+  int slots = 3;                      // CVG_SLOTS: workspaces used by host-buffer calls (1..kSlots)
+  const char* trace_path = nullptr;   // CVG_TRACE: per-block (kernel, smid, start, end)
   DevBuf<unsigned long long> trace_d, trace_s;
-  cudaStream_t main_for_join = nullptr;
-  int shallow_mode = 0;                // 0 plain (thread per column), 2 TMA-staged tiles
-  bool pairs = false;                  // deep: two columns per warp (ILP 4)
-  int shallow_persist = 0;             // overlap: persistent shallow blocks per SM (0 = grid of tiles)
   // per-kernel profiling (cvg_profile_begin/end)
   bool prof_on = false;
   int prof_cap = 0, prof_n = 0;
-  std::vector<cudaEvent_t> prof_ev;  // 5 per step: start, after trigger, after deep (main stream), shallow start/end (side)
-  int prof_mask_first = 0;
+  std::vector<cudaEvent_t> prof_ev;  // 4 per call: start, after trigger, after deep, after shallow
   // last async call
   int last_mask = 0;
   int last_maxit = 100;
@@ -172,14 +212,15 @@ void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
   CVG_CUDA(cudaGetLastError());
 }
 
+// deep kernel on `st`, then the shallow(+zero-fill) kernel: concurrently on
+// the workspace's side stream in overlap mode (the FP64-bound and the
+// HBM-bound kernel share the SMs), else after it on `st`.
 template <int VAR>
-void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh, bool dp,
-                  cudaEvent_t* pe, cudaStream_t st) {
-  // overlap: the FP64-bound deep kernel (one 20-warp block per SM, launched
-  // first) and the HBM-bound shallow kernel (forked onto the side stream,
-  // its blocks fill the rest of each SM) run concurrently
+void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh,
+                    bool dp, cudaEvent_t* pe, cudaStream_t st) {
   const bool ov = ctx->overlap && dp;
-  if (ov) CVG_CUDA(cudaEventRecord(ctx->ev_fork, st));
+  const cudaStream_t main = st;
+  if (ov) CVG_CUDA(cudaEventRecord(w.ev_fork, st));
   if (dp) {
     if (ctx->pairs && a.L <= 32) {
       if (ov) launch_deep_t<VAR, true, 14, true>(ctx, a, st);
@@ -194,16 +235,10 @@ void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowAr
   }
   if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
   if (ov) {
-    CVG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    st = ctx->side;
+    CVG_CUDA(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
+    st = w.side;
   }
-  if (ov && ctx->shallow_persist > 0) {
-    auto k = sh && dp ? cvg::shallow_persistent_kernel<VAR, true, true>
-                      : sh ? cvg::shallow_persistent_kernel<VAR, true, false>
-                           : cvg::shallow_persistent_kernel<VAR, false, true>;
-    CVG_CUDA(cudaMemsetAsync(ctx->cursor.p + 40, 0, sizeof(unsigned long long), st));
-    k<<<ctx->num_sms * ctx->shallow_persist, cvg::kShallowThreads, 0, st>>>(b, ctx->cursor.p + 40);
-  } else if (ctx->shallow_mode == 2 && (b.ld_in % 2) == 0) {
+  if (ctx->shallow_mode == 2 && (b.ld_in % 2) == 0) {
     const size_t smem = (size_t)cvg::kExpTableSize * sizeof(double2) +
                         (size_t)2 * 2 * b.L * cvg::kShTile * sizeof(double);
     auto k = sh && dp ? cvg::shallow_tma_kernel<VAR, true, true>
@@ -212,50 +247,44 @@ void launch_split(cvg_context* ctx, const cvg::DeepArgs& a, const cvg::ShallowAr
     k<<<ctx->num_sms, cvg::kShTile, smem, st>>>(b);
   } else {
     const unsigned blocks = (unsigned)((b.n + cvg::kShallowThreads - 1) / cvg::kShallowThreads);
-    CVG_CUDA(cudaFuncSetAttribute(cvg::shallow_kernel<VAR, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    if (ctx->shallow_minb == 10 && sh && dp)
-      cvg::shallow_kernel<VAR, true, true, 10><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
-    else if (sh && dp) cvg::shallow_kernel<VAR, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    if (sh && dp) cvg::shallow_kernel<VAR, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
     else if (sh) cvg::shallow_kernel<VAR, true, false><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
     else if (dp) cvg::shallow_kernel<VAR, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
   }
   CVG_CUDA(cudaGetLastError());
+  if (pe) CVG_CUDA(cudaEventRecord(pe[3], st));
   if (ov) {
-    if (pe) CVG_CUDA(cudaEventRecord(pe[3], st));
-    CVG_CUDA(cudaEventRecord(ctx->ev_join, st));
-    CVG_CUDA(cudaStreamWaitEvent(ctx->main_for_join, ctx->ev_join, 0));
+    CVG_CUDA(cudaEventRecord(w.ev_join, st));
+    CVG_CUDA(cudaStreamWaitEvent(main, w.ev_join, 0));
   }
 }
 
-// Enqueues the hot path on `st`: memsets of the per-call cursors and
-// failure words, the trigger + compaction kernel (deep requested), then the
-// deep kernel and the shallow(+zero-fill) kernel -- concurrently on a forked
-// side stream in overlap mode (the default).  Pointers are device pointers.
-void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int mask,
-             const cvg_outputs* deep, const cvg_outputs* sh, cudaStream_t st) {
+// Enqueues the hot path on `st` with workspace `w`: memsets of the per-call
+// cursors and failure words, the trigger + compaction kernel (deep
+// requested), then the deep and shallow kernels.  Pointers are device
+// pointers.  pe: optional 4 profiling events.
+void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_options* o, int mask,
+             const cvg_outputs* deep, const cvg_outputs* sh, cudaStream_t st, cudaEvent_t* pe) {
   const long long n = in->n_columns;
   const int L = in->n_levels;
-  CVG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(int), st));
-  CVG_CUDA(cudaMemsetAsync(ctx->cursor.p, 0, sizeof(unsigned long long), st));
-  CVG_CUDA(cudaMemsetAsync(ctx->err.p, 0xff, 2 * sizeof(unsigned long long), st));
+  CVG_CUDA(cudaMemsetAsync(w.counters.p, 0, 4 * sizeof(int), st));
+  CVG_CUDA(cudaMemsetAsync(w.cursor.p, 0, sizeof(unsigned long long), st));
+  CVG_CUDA(cudaMemsetAsync(w.err.p, 0xff, 2 * sizeof(unsigned long long), st));
   if (n == 0) return;
   const bool do_deep = (mask & CVG_DEEP) != 0, do_sh = (mask & CVG_SHALLOW) != 0;
-  cudaEvent_t* pe = nullptr;
-  if (ctx->prof_on && ctx->prof_n < ctx->prof_cap) pe = &ctx->prof_ev[4 * ctx->prof_n++];
   if (pe) CVG_CUDA(cudaEventRecord(pe[0], st));
   cvg::DeepArgs a{};
   if (do_deep) {
-    ctx->idx.ensure((size_t)n);
+    w.idx.ensure((size_t)n);
     const unsigned tb = (unsigned)((n + cvg::kTrigTile - 1) / cvg::kTrigTile);
-    cvg::trigger_compact_kernel<<<tb, cvg::kTrigThreads, 0, st>>>(
-        in->s, n, o->activity_threshold, ctx->idx.p, ctx->counters.p, ctx->err.p);
+    cvg::trigger_compact_kernel<<<tb, cvg::kTrigThreads, 0, st>>>(in->s, n, o->activity_threshold, w.idx.p,
+                                                                   w.counters.p, w.err.p);
     CVG_CUDA(cudaGetLastError());
     a.s = in->s; a.T = in->T; a.q = in->q; a.ld_in = in->ld;
     a.tend_T = deep->tend_T; a.tend_q = deep->tend_q; a.precip = deep->precip;
     a.work = deep->work_units; a.exited = deep->exited_early; a.ld_out = deep->ld;
-    a.idx = ctx->idx.p; a.count = ctx->counters.p;
-    a.cursor = ctx->cursor.p;
-    a.err = ctx->err.p; a.first_col = in->first_col;
+    a.idx = w.idx.p; a.count = w.counters.p; a.cursor = w.cursor.p;
+    a.err = w.err.p; a.first_col = in->first_col;
     a.thr = o->activity_threshold; a.tol = o->newton_tol; a.maxit = o->newton_max_iter;
     a.L = L;
     a.batch = std::max(1, std::min(cvg::kDeepBatch, (int)(98304 / ((size_t)cvg::kDeepWarps * L * sizeof(double)))));
@@ -273,9 +302,9 @@ void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int 
     b.d_tend_T = deep->tend_T; b.d_tend_q = deep->tend_q; b.d_precip = deep->precip;
     b.d_work = deep->work_units; b.d_exited = deep->exited_early; b.d_ld_out = deep->ld;
   }
-  b.err = ctx->err.p + 1; b.exp_tab = ctx->exp_tab.p; b.first_col = in->first_col;
+  b.err = w.err.p + 1; b.exp_tab = ctx->exp_tab.p; b.first_col = in->first_col;
   b.thr = o->activity_threshold; b.L = L;
-  if (ctx->trace_path) {
+  if (ctx->trace_path && &w == &ctx->ws[0]) {
     ctx->trace_d.ensure(3 * 4096);
     ctx->trace_s.ensure(3 * (size_t)((n + 127) / 128 + 1));
     CVG_CUDA(cudaMemsetAsync(ctx->trace_d.p, 0, 3 * 4096 * 8, st));
@@ -283,22 +312,27 @@ void enqueue(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int 
     a.trace = ctx->trace_d.p;
     b.trace = ctx->trace_s.p;
   }
-  ctx->main_for_join = st;
   switch (o->variant) {
-    case 1: launch_split<cvg::kVarReduced>(ctx, a, b, do_sh, do_deep, pe, st); break;
-    case 2: launch_split<cvg::kVarApprox>(ctx, a, b, do_sh, do_deep, pe, st); break;
-    default: launch_split<cvg::kVarExact>(ctx, a, b, do_sh, do_deep, pe, st); break;
+    case 1: launch_kernels<cvg::kVarReduced>(ctx, w, a, b, do_sh, do_deep, pe, st); break;
+    case 2: launch_kernels<cvg::kVarApprox>(ctx, w, a, b, do_sh, do_deep, pe, st); break;
+    default: launch_kernels<cvg::kVarExact>(ctx, w, a, b, do_sh, do_deep, pe, st); break;
   }
-  if (pe && !(ctx->overlap && do_deep)) CVG_CUDA(cudaEventRecord(pe[3], st));
 }
 
-// Reads back the latched failure words (stream already synchronised).
-cvg_status collect(cvg_context* ctx, int mask, int maxit, long long n, cvg_stats* stats) {
-  CVG_CUDA(cudaMemcpy(ctx->h_err, ctx->err.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-  CVG_CUDA(cudaMemcpy(ctx->h_count, ctx->counters.p, sizeof(int), cudaMemcpyDeviceToHost));
+// Queues the D2H of a workspace's latched failure words / trigger count.
+void read_flags_async(Workspace& w, cudaStream_t st) {
+  CVG_CUDA(cudaMemcpyAsync(w.h_err, w.err.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CVG_CUDA(cudaMemcpyAsync(w.h_count, w.counters.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+}
+
+// Turns the folded failure keys (minimum over the call's chunks) into the
+// reference's error: deep first, then shallow, as the reference runs
+// deep_convection then shallow_convection; the lowest failing column.
+cvg_status collect(const unsigned long long* keys_deep, const unsigned long long* keys_sh, long long triggered,
+                   int mask, int maxit, long long n, cvg_stats* stats) {
   if (stats) {
     stats->n_columns = n;
-    stats->n_triggered = (mask & CVG_DEEP) ? *ctx->h_count : 0;
+    stats->n_triggered = (mask & CVG_DEEP) ? triggered : 0;
     stats->failing_column = -1;
     stats->failure_kind = 0;
     stats->failing_kernel = 0;
@@ -307,7 +341,7 @@ cvg_status collect(cvg_context* ctx, int mask, int maxit, long long n, cvg_stats
   for (int w = 0; w < 2; ++w) {
     const int kernel = w == 0 ? CVG_DEEP : CVG_SHALLOW;
     if (!(mask & kernel)) continue;
-    const unsigned long long key = ctx->h_err[w];
+    const unsigned long long key = w == 0 ? *keys_deep : *keys_sh;
     if (key == none) continue;
     const long long col = (long long)(key >> 16);
     const int kind = (int)(key & 7);
@@ -360,7 +394,7 @@ void copy_rows_d2h(double* dst, long long ld, const double* src, long long n, in
 
 extern "C" {
 
-const char* cvg_version(void) { return "0.1.0"; }
+const char* cvg_version(void) { return "0.2.0"; }
 
 const char* cvg_last_error(void) { return g_last_error.c_str(); }
 
@@ -392,34 +426,21 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     auto* ctx = new cvg_context();
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
+    if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
+    if (const char* e = getenv("CVG_PAIRS")) ctx->pairs = atoi(e) != 0;
+    if (const char* e = getenv("CVG_SHALLOW_MODE")) ctx->shallow_mode = atoi(e);
+    if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
+    if (const char* e = getenv("CVG_SLOTS")) ctx->slots = std::max(1, std::min(kSlots, atoi(e)));
+    ctx->trace_path = getenv("CVG_TRACE");
     try {
       CVG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-      CVG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
-      CVG_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-      CVG_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
-      CVG_CUDA(cudaEventCreate(&ctx->ev0));
-      CVG_CUDA(cudaEventCreate(&ctx->ev1));
-      CVG_CUDA(cudaEventCreate(&ctx->ev_h0));
-      CVG_CUDA(cudaEventCreate(&ctx->ev_h1));
-      CVG_CUDA(cudaEventCreate(&ctx->ev_d0));
+      for (cudaEvent_t* e : {&ctx->ev0, &ctx->ev1, &ctx->ev_h0, &ctx->ev_h1}) CVG_CUDA(cudaEventCreate(e));
       const std::vector<double2> tab = exp_table_host();
       ctx->exp_tab.ensure(tab.size());
       CVG_CUDA(cudaMemcpy(ctx->exp_tab.p, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
-      ctx->counters.ensure(4);
-      ctx->cursor.ensure(80);  // [0] deep cursor, [40] tile cursor, others dummies
-      CVG_CUDA(cudaMemset(ctx->cursor.p, 0, 80 * sizeof(unsigned long long)));
-      ctx->err.ensure(4);
-      CVG_CUDA(cudaMallocHost(&ctx->h_err, 4 * sizeof(unsigned long long)));
-      CVG_CUDA(cudaMallocHost(&ctx->h_count, 4 * sizeof(int)));
-      CVG_CUDA(cudaMemset(ctx->counters.p, 0, 4 * sizeof(int)));
-      CVG_CUDA(cudaMemset(ctx->err.p, 0xff, 4 * sizeof(unsigned long long)));
-      // probe that the sm_100a image loads on this device
-      if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
-      if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
-      ctx->trace_path = getenv("CVG_TRACE");
-      if (const char* e = getenv("CVG_SHALLOW_MODE")) ctx->shallow_mode = atoi(e);
-      if (const char* e = getenv("CVG_PAIRS")) ctx->pairs = atoi(e) != 0;
-      if (const char* e = getenv("CVG_SHALLOW_PERSIST")) ctx->shallow_persist = atoi(e);
+      for (Workspace& w : ctx->ws) w.create();
+      ctx->aux_err.ensure(1);
+      CVG_CUDA(cudaMallocHost(&ctx->h_aux_err, sizeof(unsigned long long)));
     } catch (...) {
       cvg_context_free(ctx);
       throw;
@@ -432,29 +453,20 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
 void cvg_context_free(cvg_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  for (auto* b : {&ctx->exp_tab}) b->release();
-  ctx->idx.release();
-  ctx->counters.release();
-  ctx->cursor.release();
-  ctx->err.release();
-  for (auto* b : {&ctx->in_s, &ctx->in_T, &ctx->in_q, &ctx->dT, &ctx->dq, &ctx->dp, &ctx->sT, &ctx->sq, &ctx->sp,
-                  &ctx->aux0, &ctx->aux1})
-    b->release();
-  ctx->dw.release();
-  ctx->sw.release();
-  ctx->dx.release();
-  ctx->sx.release();
+  cudaDeviceSynchronize();
+  ctx->exp_tab.release();
+  for (Workspace& w : ctx->ws) w.destroy();
+  ctx->aux0.release();
+  ctx->aux1.release();
   ctx->auxi.release();
-  if (ctx->h_err) cudaFreeHost(ctx->h_err);
-  if (ctx->h_count) cudaFreeHost(ctx->h_count);
-  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->ev_h0, ctx->ev_h1, ctx->ev_d0})
+  ctx->aux_err.release();
+  ctx->trace_d.release();
+  ctx->trace_s.release();
+  if (ctx->h_aux_err) cudaFreeHost(ctx->h_aux_err);
+  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->ev_h0, ctx->ev_h1})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
-  if (ctx->side) cudaStreamDestroy(ctx->side);
-  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 
@@ -473,7 +485,9 @@ cvg_status cvg_convect_async(cvg_context* ctx, const cvg_columns* in, const cvg_
   return guarded([&] {
     CVG_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    enqueue(ctx, in, opts, mask, deep, sh, st);
+    cudaEvent_t* pe = nullptr;
+    if (ctx->prof_on && ctx->prof_n < ctx->prof_cap) pe = &ctx->prof_ev[4 * ctx->prof_n++];
+    enqueue(ctx, ctx->ws[0], in, opts, mask, deep, sh, st, pe);
     ctx->last_mask = mask;
     ctx->last_maxit = opts->newton_max_iter;
     ctx->last_n = in->n_columns;
@@ -490,6 +504,9 @@ cvg_status cvg_convect_check(cvg_context* ctx, void* stream, cvg_stats* stats) {
     CVG_CUDA(cudaStreamSynchronize(st));
     if (stats) std::memset(stats, 0, sizeof(*stats));
     if (!ctx->pending) return CVG_OK;
+    Workspace& w = ctx->ws[0];
+    read_flags_async(w, st);
+    CVG_CUDA(cudaStreamSynchronize(st));
     if (ctx->trace_path && ctx->trace_d.p) {
       const size_t nd = 3 * 4096, ns = 3 * (size_t)((ctx->last_n + 127) / 128 + 1);
       std::vector<unsigned long long> hd(nd), hs(ns);
@@ -503,10 +520,18 @@ cvg_status cvg_convect_check(cvg_context* ctx, void* stream, cvg_stats* stats) {
         fclose(f);
       }
     }
-    return collect(ctx, ctx->last_mask, ctx->last_maxit, ctx->last_n, stats);
+    return collect(&w.h_err[0], &w.h_err[1], *w.h_count, ctx->last_mask, ctx->last_maxit, ctx->last_n, stats);
   });
 }
 
+// Host-buffer (or mixed) call.  Column chunks of chunk_cols columns are
+// pipelined through the kSlots workspaces, each on its own stream: chunk i's
+// H2D, chunk i-1's kernels and chunk i-2's D2H run concurrently (two copy
+// engines, full-duplex PCIe), so a host-buffer call costs roughly its larger
+// transfer direction rather than the sum of transfers and compute.  Results
+// equal a single-chunk call bit for bit: columns are independent and every
+// failure key carries the absolute column id, so the lowest failing column
+// is the minimum over chunks.  All-device calls run as one chunk.
 cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_options* opts, int mask,
                        const cvg_outputs* deep, const cvg_outputs* sh, cvg_stats* stats) {
   if (!ctx || !in || !opts) return fail(CVG_ERR_INVALID, "cvg_convect: null argument");
@@ -519,68 +544,104 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
     return fail(CVG_ERR_INVALID, "cvg_convect: shallow outputs: " + (sh ? why : std::string("null")));
   return guarded([&] {
     CVG_CUDA(cudaSetDevice(ctx->device));
-    cudaStream_t st = ctx->stream;
     const long long n = in->n_columns;
     const int L = in->n_levels;
-    const size_t nL = (size_t)n * L;
-    long long h2d = 0, d2h = 0;
-    // ---- stage inputs
-    cvg_columns din = *in;
-    CVG_CUDA(cudaEventRecord(ctx->ev_h0, st));
-    if (!in->on_device && n > 0) {
-      ctx->in_s.ensure(n);
-      ctx->in_T.ensure(nL);
-      ctx->in_q.ensure(nL);
-      CVG_CUDA(cudaMemcpyAsync(ctx->in_s.p, in->s, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-      copy_rows_h2d(ctx->in_T.p, in->T, n, L, in->ld, st);
-      copy_rows_h2d(ctx->in_q.p, in->q, n, L, in->ld, st);
-      h2d = (long long)(sizeof(double) * (n + 2 * nL));
-      din.s = ctx->in_s.p;
-      din.T = ctx->in_T.p;
-      din.q = ctx->in_q.p;
-      din.ld = n;
-      din.on_device = 1;
-    }
-    auto stage_out = [&](const cvg_outputs* o, DevBuf<double>& T, DevBuf<double>& q, DevBuf<double>& p,
-                         DevBuf<long long>& w, DevBuf<uint8_t>& x) {
-      cvg_outputs d = *o;
-      if (!o->on_device && n > 0) {
-        T.ensure(nL); q.ensure(nL); p.ensure(n); w.ensure(n); x.ensure(n);
-        d.tend_T = T.p; d.tend_q = q.p; d.precip = p.p; d.work_units = w.p; d.exited_early = x.p;
-        d.ld = n; d.on_device = 1;
+    const bool all_dev = in->on_device && (!(mask & CVG_DEEP) || deep->on_device) &&
+                         (!(mask & CVG_SHALLOW) || sh->on_device);
+    // chunk boundaries: the first chunks ramp up geometrically from
+    // chunk_cols/8 so the D2H stream (the larger direction) starts early
+    std::vector<long long> bounds{0};
+    if (all_dev || n == 0) {
+      bounds.push_back(n);
+    } else {
+      long long c = std::max(1LL, ctx->chunk_cols / 8);
+      while (bounds.back() < n) {
+        bounds.push_back(std::min(n, bounds.back() + c));
+        c = std::min(ctx->chunk_cols, 2 * c);
       }
-      return d;
+    }
+    const long long nchunks = (long long)bounds.size() - 1;
+    long long h2d = 0, d2h = 0;
+    CVG_CUDA(cudaEventRecord(ctx->ev_h0, ctx->stream));
+    unsigned long long md = ~0ULL, ms_ = ~0ULL;
+    long long trig = 0;
+    bool busy[kSlots] = {};
+    auto drain = [&](Workspace& w) {  // a slot's previous chunk: wait, fold its flags
+      CVG_CUDA(cudaStreamSynchronize(w.stream));
+      md = std::min(md, w.h_err[0]);
+      ms_ = std::min(ms_, w.h_err[1]);
+      trig += *w.h_count;
     };
-    cvg_outputs ddeep{}, dsh{};
-    if (mask & CVG_DEEP) ddeep = stage_out(deep, ctx->dT, ctx->dq, ctx->dp, ctx->dw, ctx->dx);
-    if (mask & CVG_SHALLOW) dsh = stage_out(sh, ctx->sT, ctx->sq, ctx->sp, ctx->sw, ctx->sx);
-    CVG_CUDA(cudaEventRecord(ctx->ev0, st));
-    enqueue(ctx, &din, opts, mask, &ddeep, &dsh, st);
-    CVG_CUDA(cudaEventRecord(ctx->ev1, st));
-    // ---- outputs back
-    auto unstage = [&](const cvg_outputs* o, const cvg_outputs& d) {
-      if (o->on_device || n == 0) return;
-      copy_rows_d2h(o->tend_T, o->ld, d.tend_T, n, L, st);
-      copy_rows_d2h(o->tend_q, o->ld, d.tend_q, n, L, st);
-      CVG_CUDA(cudaMemcpyAsync(o->precip, d.precip, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-      CVG_CUDA(cudaMemcpyAsync(o->work_units, d.work_units, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
-      CVG_CUDA(cudaMemcpyAsync(o->exited_early, d.exited_early, n, cudaMemcpyDeviceToHost, st));
-      d2h += (long long)(sizeof(double) * (2 * nL + n) + sizeof(long long) * n + n);
-    };
-    if (mask & CVG_DEEP) unstage(deep, ddeep);
-    if (mask & CVG_SHALLOW) unstage(sh, dsh);
-    CVG_CUDA(cudaEventRecord(ctx->ev_h1, st));
-    CVG_CUDA(cudaStreamSynchronize(st));
-    cvg_status rc = collect(ctx, mask, opts->newton_max_iter, n, stats);
+    for (long long ci = 0; ci < nchunks; ++ci) {
+      const int slot = (int)(ci % ctx->slots);
+      Workspace& w = ctx->ws[slot];
+      if (busy[slot]) drain(w);
+      CVG_CUDA(cudaStreamWaitEvent(w.stream, ctx->ev_h0, 0));
+      const long long c0 = bounds[ci];
+      const long long m = bounds[ci + 1] - c0;
+      const size_t mL = (size_t)m * L;
+      cvg_columns din = *in;
+      din.n_columns = m;
+      din.first_col = in->first_col + c0;
+      if (in->on_device) {
+        if (m > 0) { din.s = in->s + c0; din.T = in->T + c0; din.q = in->q + c0; }
+      } else if (m > 0) {
+        w.in_s.ensure(m); w.in_T.ensure(mL); w.in_q.ensure(mL);
+        CVG_CUDA(cudaMemcpyAsync(w.in_s.p, in->s + c0, sizeof(double) * m, cudaMemcpyHostToDevice, w.stream));
+        copy_rows_h2d(w.in_T.p, in->T + c0, m, L, in->ld, w.stream);
+        copy_rows_h2d(w.in_q.p, in->q + c0, m, L, in->ld, w.stream);
+        h2d += (long long)(sizeof(double) * (m + 2 * mL));
+        din.s = w.in_s.p; din.T = w.in_T.p; din.q = w.in_q.p; din.ld = m; din.on_device = 1;
+      }
+      auto stage = [&](const cvg_outputs* o, DevBuf<double>& T, DevBuf<double>& q, DevBuf<double>& p,
+                       DevBuf<long long>& wk, DevBuf<uint8_t>& x) {
+        cvg_outputs d = *o;
+        if (o->on_device) {
+          if (m > 0) {
+            d.tend_T = o->tend_T + c0; d.tend_q = o->tend_q + c0; d.precip = o->precip + c0;
+            d.work_units = o->work_units + c0; d.exited_early = o->exited_early + c0;
+          }
+        } else if (m > 0) {
+          T.ensure(mL); q.ensure(mL); p.ensure(m); wk.ensure(m); x.ensure(m);
+          d.tend_T = T.p; d.tend_q = q.p; d.precip = p.p; d.work_units = wk.p; d.exited_early = x.p;
+          d.ld = m; d.on_device = 1;
+        }
+        return d;
+      };
+      cvg_outputs ddeep{}, dsh{};
+      if (mask & CVG_DEEP) ddeep = stage(deep, w.dT, w.dq, w.dp, w.dw, w.dx);
+      if (mask & CVG_SHALLOW) dsh = stage(sh, w.sT, w.sq, w.sp, w.sw, w.sx);
+      enqueue(ctx, w, &din, opts, mask, &ddeep, &dsh, w.stream, nullptr);
+      auto unstage = [&](const cvg_outputs* o, const cvg_outputs& d) {
+        if (o->on_device || m <= 0) return;
+        copy_rows_d2h(o->tend_T + c0, o->ld, d.tend_T, m, L, w.stream);
+        copy_rows_d2h(o->tend_q + c0, o->ld, d.tend_q, m, L, w.stream);
+        CVG_CUDA(cudaMemcpyAsync(o->precip + c0, d.precip, sizeof(double) * m, cudaMemcpyDeviceToHost, w.stream));
+        CVG_CUDA(cudaMemcpyAsync(o->work_units + c0, d.work_units, sizeof(long long) * m, cudaMemcpyDeviceToHost,
+                                 w.stream));
+        CVG_CUDA(cudaMemcpyAsync(o->exited_early + c0, d.exited_early, m, cudaMemcpyDeviceToHost, w.stream));
+        d2h += (long long)(sizeof(double) * (2 * mL + m) + sizeof(long long) * m + m);
+      };
+      if (mask & CVG_DEEP) unstage(deep, ddeep);
+      if (mask & CVG_SHALLOW) unstage(sh, dsh);
+      read_flags_async(w, w.stream);
+      busy[slot] = true;
+    }
+    for (int s = 0; s < kSlots; ++s)
+      if (busy[s]) drain(ctx->ws[s]);
+    cvg_status rc = collect(&md, &ms_, trig, mask, opts->newton_max_iter, n, stats);
     if (stats) {
-      float ms = 0.f, all = 0.f;
-      CVG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+      for (int s = 0; s < kSlots; ++s) {
+        CVG_CUDA(cudaEventRecord(ctx->ev1, ctx->ws[s].stream));
+        CVG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev1, 0));
+      }
+      CVG_CUDA(cudaEventRecord(ctx->ev_h1, ctx->stream));
+      CVG_CUDA(cudaEventSynchronize(ctx->ev_h1));
+      float all = 0.f;
       CVG_CUDA(cudaEventElapsedTime(&all, ctx->ev_h0, ctx->ev_h1));
-      stats->device_ms = ms;
-      float h = 0.f;
-      CVG_CUDA(cudaEventElapsedTime(&h, ctx->ev_h0, ctx->ev0));
-      stats->h2d_ms = h;
-      stats->d2h_ms = std::max(0.f, all - ms - h);
+      stats->device_ms = all;   // whole call, transfers overlapped with compute
+      stats->h2d_ms = 0.0;
+      stats->d2h_ms = 0.0;
       stats->h2d_bytes = h2d;
       stats->d2h_bytes = d2h;
     }
@@ -616,20 +677,20 @@ cvg_status cvg_ientropy_solve(cvg_context* ctx, long long n, const double* y, co
     double* dg = ctx->aux1.p + n;
     CVG_CUDA(cudaMemcpyAsync(dy, y, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     CVG_CUDA(cudaMemcpyAsync(dg, guess, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-    CVG_CUDA(cudaMemsetAsync(ctx->err.p + 2, 0xff, sizeof(unsigned long long), st));
+    CVG_CUDA(cudaMemsetAsync(ctx->aux_err.p, 0xff, sizeof(unsigned long long), st));
     const unsigned blocks = (unsigned)((n + 255) / 256);
     switch (opts->variant) {
       case 2: cvg::ientropy_kernel<cvg::kVarApprox><<<blocks, 256, 0, st>>>(dy, dg, n, opts->newton_tol,
-                  opts->newton_max_iter, ctx->aux0.p, ctx->auxi.p, ctx->err.p + 2, ctx->exp_tab.p); break;
+                  opts->newton_max_iter, ctx->aux0.p, ctx->auxi.p, ctx->aux_err.p, ctx->exp_tab.p); break;
       default: cvg::ientropy_kernel<cvg::kVarExact><<<blocks, 256, 0, st>>>(dy, dg, n, opts->newton_tol,
-                  opts->newton_max_iter, ctx->aux0.p, ctx->auxi.p, ctx->err.p + 2, ctx->exp_tab.p); break;
+                  opts->newton_max_iter, ctx->aux0.p, ctx->auxi.p, ctx->aux_err.p, ctx->exp_tab.p); break;
     }
     CVG_CUDA(cudaGetLastError());
     CVG_CUDA(cudaMemcpyAsync(root, ctx->aux0.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     CVG_CUDA(cudaMemcpyAsync(iterations, ctx->auxi.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
-    CVG_CUDA(cudaMemcpyAsync(ctx->h_err + 2, ctx->err.p + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CVG_CUDA(cudaMemcpyAsync(ctx->h_aux_err, ctx->aux_err.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CVG_CUDA(cudaStreamSynchronize(st));
-    const unsigned long long key = ctx->h_err[2];
+    const unsigned long long key = *ctx->h_aux_err;
     if (key != ~0ULL) {
       std::string buf;
       const char* what = kind_message((int)(key & 7), CVG_DEEP, opts->newton_max_iter, &buf);

@@ -865,53 +865,6 @@ __global__ void __launch_bounds__(kShallowThreads, MINB) shallow_kernel(ShallowA
 }
 
 // ---------------------------------------------------------------------------
-// Persistent shallow(+zero-fill) kernel for overlap mode: NB blocks of 128
-// threads per SM share the SMs with the deep kernel's blocks.  A block walks
-// 128-column tiles (dynamic cursor, one claim per tile, issued a tile
-// ahead) and, while it computes tile t, asks the TMA engine to prefetch
-// tile t+1's 2 L rows into L2 (cp.async.bulk.prefetch), so its per-thread
-// row loads are L2 hits: the shallow work then needs little issue share to
-// keep pace with the FP64-bound deep kernel beside it.
-template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO>
-__global__ void __launch_bounds__(kShallowThreads) shallow_persistent_kernel(ShallowArgs a,
-                                                                           unsigned long long* cursor) {
-  __shared__ double2 s_tab[kExpTableSize];
-  __shared__ long long s_next;
-  if (DO_SHALLOW && VAR != kVarApprox) {
-    for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
-  }
-  const int L = a.L;
-  const long long ntiles = (a.n + kShallowThreads - 1) / kShallowThreads;
-  const bool can_prefetch = DO_SHALLOW && (a.ld_in & 1) == 0;
-  auto prefetch = [&](long long tile) {
-    if (!can_prefetch || tile >= ntiles) return;
-    const long long c0 = tile * kShallowThreads;
-    const long long cols = min((long long)kShallowThreads, a.n - c0);
-    const unsigned bytes = (unsigned)((cols * 8 + 15) & ~15LL);
-    if (c0 + bytes / 8 > a.ld_in) return;
-    for (int k = (int)threadIdx.x; k < 2 * L; k += blockDim.x) {
-      const double* base = (k < L ? a.T + (long long)k * a.ld_in : a.q + (long long)(k - L) * a.ld_in) + c0;
-      bulk_prefetch_l2(base, bytes);
-    }
-  };
-  if (threadIdx.x == 0) s_next = (long long)atomicAdd(cursor, 1ULL);
-  __syncthreads();
-  long long tile = s_next;
-  __syncthreads();
-  if (threadIdx.x == 0) s_next = (long long)atomicAdd(cursor, 1ULL);
-  prefetch(tile);
-  while (tile < ntiles) {
-    __syncthreads();
-    const long long nxt = s_next;
-    __syncthreads();
-    if (threadIdx.x == 0 && nxt < ntiles) s_next = (long long)atomicAdd(cursor, 1ULL);
-    prefetch(nxt);
-    const long long c = tile * kShallowThreads + threadIdx.x;
-    if (c < a.n) shallow_column<VAR, DO_SHALLOW, DO_DEEP_ZERO, 1>(a, c, s_tab);
-    tile = nxt;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Streaming shallow(+zero-fill) kernel on the TMA engine: one persistent
 // block per SM walks tiles of kShTile columns; thread 0 stages the next

@@ -169,3 +169,85 @@ def test_device_resident_async_path(ctx):
     with pytest.raises(P.KernelError) as e:
         ctx.check(stream)
     assert e.value.column == 7
+
+
+@pytest.fixture(scope="module")
+def small_chunk_ctx():
+    """A context whose host-buffer calls pipeline 1000-column chunks, so a
+    few thousand columns cross several chunks and reuse every workspace slot."""
+    import os
+    old = os.environ.get("CVG_CHUNK_COLS")
+    os.environ["CVG_CHUNK_COLS"] = "1000"
+    try:
+        c = P.Context(0)
+    finally:
+        if old is None:
+            del os.environ["CVG_CHUNK_COLS"]
+        else:
+            os.environ["CVG_CHUNK_COLS"] = old
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("n", [999, 1000, 1001, 7777])
+def test_chunked_pipeline_matches_single_chunk(ctx, small_chunk_ctx, n):
+    s, T, q = G.make_config("c1", n=n, seed=n)
+    for v in (0, 2):
+        o = P.KernelOptions(variant=v)
+        d1, s1 = ctx.convect(s, T, q, o, first_col=50)
+        d2, s2 = small_chunk_ctx.convect(s, T, q, o, first_col=50)
+        for a, b in ((d1, d2), (s1, s2)):
+            for f in ("tend_T", "tend_q", "precip", "work_units", "exited_early"):
+                assert np.array_equal(getattr(a, f), getattr(b, f), equal_nan=True), f
+        assert small_chunk_ctx.last_stats.n_triggered == int((s > 0.5).sum())
+        assert small_chunk_ctx.last_stats.h2d_bytes == 8 * n * (1 + 2 * T.shape[0])
+
+
+def test_chunked_pipeline_error_is_lowest_column_over_chunks(small_chunk_ctx):
+    s, T, q = G.make_config("c1", n=5000, seed=3)
+    active = np.nonzero(s > 0.5)[0]
+    late, early = int(active[active > 4000][0]), int(active[(active > 1000) & (active < 2000)][0])
+    T[2, late] = np.nan
+    with pytest.raises(P.KernelError) as e:
+        small_chunk_ctx.deep_convection(s, T, q, first_col=7)
+    assert e.value.column == late + 7
+    T[5, early] = np.inf
+    with pytest.raises(P.KernelError) as e:
+        small_chunk_ctx.deep_convection(s, T, q, first_col=7)
+    assert e.value.column == early + 7
+    # a deep failure is reported before a shallow one even when the shallow
+    # failure sits in an earlier chunk (the reference runs deep first)
+    s[10] = np.nan
+    with pytest.raises(P.KernelError) as e:
+        small_chunk_ctx.convect(s, T, q)
+    assert e.value.column == 10 and "deep: non-finite activity" in str(e.value)
+    s[10] = 0.1
+    with pytest.raises(P.KernelError) as e:
+        small_chunk_ctx.convect(s, T, q)
+    assert e.value.column == early and "ientropy" in str(e.value)
+    s[early - 1] = np.inf
+    with pytest.raises(P.KernelError) as e:
+        small_chunk_ctx.shallow_convection(s, T, q)
+    assert e.value.column == early - 1 and "shallow" in str(e.value)
+    # and the context is usable afterwards
+    s, T, q = G.make_config("c1", n=3000, seed=4)
+    both_close(small_chunk_ctx.deep_convection(s, T, q), O.convection("deep", s, T, q))
+
+
+def test_chunked_pipeline_strided_host_rows(small_chunk_ctx):
+    s, T, q = G.make_config("c1", n=3500, seed=5)
+    n, L = 3200, T.shape[0]
+    lib = P.load_library()
+    cols = P._Columns(n, L, 0, T.shape[1], s.ctypes.data, T.ctypes.data, q.ctypes.data, 0)
+    out = P.ColumnOutputs(np.zeros((L, 3500)), np.zeros((L, 3500)), np.zeros(n), np.zeros(n, np.int64),
+                          np.zeros(n, np.uint8))
+    o = P._Outputs(out.tend_T.ctypes.data, out.tend_q.ctypes.data, out.precip.ctypes.data,
+                   out.work_units.ctypes.data, out.exited_early.ctypes.data, 3500, 0)
+    st = P.Stats()
+    rc = lib.cvg_deep_convection(small_chunk_ctx._h, C.byref(cols), C.byref(P.KernelOptions()), C.byref(o),
+                                 C.byref(st))
+    assert rc == 0
+    od = O.convection("deep", s[:n], np.ascontiguousarray(T[:, :n]), np.ascontiguousarray(q[:, :n]))
+    got = P.ColumnOutputs(out.tend_T[:, :n], out.tend_q[:, :n], out.precip, out.work_units, out.exited_early)
+    both_close(got, od)
+    assert not out.tend_T[:, n:].any()
