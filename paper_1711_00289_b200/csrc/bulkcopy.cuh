@@ -55,4 +55,27 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, unsigned 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
 }
 
+// Per-thread asynchronous global -> shared copies (LDGSTS): the data lands
+// in shared memory without occupying registers or a register scoreboard;
+// the issuing thread waits for its own copies with cp_async_wait_all.
+__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8_u32(unsigned dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst_smem), "l"(src_gmem) : "memory");
+}
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+// A shared-memory address the compiler cannot rematerialise (it would
+// otherwise recompute it from %cgactaid inside loops under register caps).
+__device__ __forceinline__ unsigned opaque_u32(unsigned x) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 }  // namespace cvg

@@ -159,6 +159,8 @@ struct cvg_context {
   bool overlap = true;     // CVG_OVERLAP: deep || shallow on two streams
   bool pairs = false;      // CVG_PAIRS: two deep columns per warp (ILP 4)
   int shallow_mode = 0;    // CVG_SHALLOW_MODE: 0 thread per column, 2 TMA-staged tiles
+  int deep_warps = 0;      // CVG_DEEP_WARPS: 12, 16 or 20 warps per deep block (0: by mode)
+  bool strict = false;     // CVG_STRICT: reference rounding in every Newton update (all variants)
   long long chunk_cols = kChunkCols;  // CVG_CHUNK_COLS: host-call pipeline chunk
   int slots = 3;                      // CVG_SLOTS: workspaces used by host-buffer calls (1..kSlots)
   const char* trace_path = nullptr;   // CVG_TRACE: per-block (kernel, smid, start, end)
@@ -222,15 +224,18 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   const cudaStream_t main = st;
   if (ov) CVG_CUDA(cudaEventRecord(w.ev_fork, st));
   if (dp) {
+    // deep block size: kDeepWarpsOverlap leaves each SM room for three
+    // shallow blocks beside the deep block; kDeepWarps when deep runs alone
+    const int nw = ctx->deep_warps > 0 ? ctx->deep_warps : (ov ? cvg::kDeepWarpsOverlap : cvg::kDeepWarps);
     if (ctx->pairs && a.L <= 32) {
-      if (ov) launch_deep_t<VAR, true, 14, true>(ctx, a, st);
-      else launch_deep_t<VAR, true, 16, true>(ctx, a, st);
-    } else if (ov) {
-      if (a.L <= 32) launch_deep_t<VAR, true, cvg::kDeepWarpsOverlap>(ctx, a, st);
-      else launch_deep_t<VAR, false, cvg::kDeepWarpsOverlap>(ctx, a, st);
+      launch_deep_t<VAR, true, 14, true>(ctx, a, st);
+    } else if (a.L <= 32) {
+      if (nw == 16) launch_deep_t<VAR, true, 16>(ctx, a, st);
+      else if (nw == 20) launch_deep_t<VAR, true, 20>(ctx, a, st);
+      else launch_deep_t<VAR, true, 12>(ctx, a, st);
     } else {
-      if (a.L <= 32) launch_deep_t<VAR, true, cvg::kDeepWarps>(ctx, a, st);
-      else launch_deep_t<VAR, false, cvg::kDeepWarps>(ctx, a, st);
+      if (nw == 16) launch_deep_t<VAR, false, 16>(ctx, a, st);
+      else launch_deep_t<VAR, false, 12>(ctx, a, st);
     }
   }
   if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
@@ -289,6 +294,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.L = L;
     a.batch = std::max(1, std::min(cvg::kDeepBatch, (int)(98304 / ((size_t)cvg::kDeepWarps * L * sizeof(double)))));
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
+    a.relaxed = !ctx->strict;
   }
   a.exp_tab = ctx->exp_tab.p;
   if (pe) CVG_CUDA(cudaEventRecord(pe[1], st));
@@ -428,6 +434,8 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     ctx->num_sms = prop.multiProcessorCount;
     if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
     if (const char* e = getenv("CVG_PAIRS")) ctx->pairs = atoi(e) != 0;
+    if (const char* e = getenv("CVG_STRICT")) ctx->strict = atoi(e) != 0;
+    if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
     if (const char* e = getenv("CVG_SHALLOW_MODE")) ctx->shallow_mode = atoi(e);
     if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
     if (const char* e = getenv("CVG_SLOTS")) ctx->slots = std::max(1, std::min(kSlots, atoi(e)));

@@ -150,6 +150,7 @@ struct DeepArgs {
   int L;                  // levels
   int batch;              // columns per precip batch (<= kDeepBatch)
   bool fast_div_ok;       // newton_tol >= 2^-500
+  bool relaxed;           // relaxed-rounding Newton update allowed (colmath.cuh)
 };
 
 // Deep-kernel lanes read a lane-private copy of the exp table (see
@@ -235,7 +236,24 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
   const bool inputs_ok = is_finite(ye) && is_finite(yp);
   const bool fast_ok = inputs_ok && a.fast_div_ok && ye > -60.0 && yp > -60.0 && ye < kBig &&
                        yp < kBig && he > 0.0 && hp > 0.0 && exp_fast_ok(mul(kMC.c005, guess));
-  if (fast_ok) {
+  if (VAR != kVarApprox && fast_ok && a.relaxed && relaxed_ok(ye, a.tol) && relaxed_ok(yp, a.tol)) {
+    // relaxed update (colmath.cuh): same iteration and stop test, rounding
+    // noise only; the exact sequence below is the one the reference runs
+    const double tol = a.tol;
+    const int maxit = a.maxit;
+    // opaque to the compiler, so the lane's table address stays in a
+    // register instead of being rematerialised from %tid inside the loop
+    unsigned tab_addr;
+    asm volatile("mov.b32 %0, %1;" : "=r"(tab_addr) : "r"((unsigned)__cvta_generic_to_shared(tab)));
+    int left = maxit + 1;   // updates still allowed (the loop may take one
+                            // more than maxit; newton_finish then fails it)
+    if (left > 0) do {
+      if (abs_le_either(he, hp, tol)) break;
+      newton_relaxed_step<kTabCopies>(te, ee, he, ye, tab_addr);
+      newton_relaxed_step<kTabCopies>(tp, ep, hp, yp, tab_addr);
+    } while (--left != 0);
+    it = maxit + 1 - max(left, 0);
+  } else if (fast_ok) {
     const double tol = a.tol;
     const int maxit = a.maxit;
     while (it <= maxit) {
@@ -277,12 +295,22 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
 constexpr int kDeepBatch = 16;
 constexpr int kDeepChunk = 4;   // list entries claimed per atomic (power of 2)
 
+// Issued by lane 0 only, at cursor + lane (= cursor): an address ptxas
+// cannot prove warp-uniform, so it does not rewrite the atomic into its
+// aggregated form (vote + one atomic + SHFL of the result), whose SHFL
+// would wait for the atomic on the spot.
+__device__ __forceinline__ long long claim_chunk(unsigned long long* cursor_plus_lane) {
+  unsigned long long r;
+  asm volatile("atom.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(cursor_plus_lane), "n"(kDeepChunk) : "memory");
+  return (long long)r;
+}
+
 // The deep role of a warp: walks the compacted list until it is exhausted.
 // s_tab points at this lane's copy of the replicated exp table; s_term is
 // this warp's [batch][L] precip scratch, s_bcol / s_bwork its batch slots.
 template <int VAR, bool NARROW>
 __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_tab, double* s_term,
-                                            int* s_bcol, int* s_bwork, int lane) {
+                                            int* s_bcol, int* s_bwork, double* s_stage, int lane) {
   const int L = a.L;
   const long long A = *a.count;
   const bool reduced = (VAR == kVarReduced);
@@ -293,16 +321,13 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
   // q[lane]) are loaded during the previous entry's solves, the entry after
   // next is known a column ahead, and the next chunk is claimed a chunk
   // ahead, so no load or atomic sits on the issue path of a column.
-  // Every lane issues the claim atomic -- lane 0 on the cursor, the others
-  // adding 0 to private dummy words -- so the addresses are not uniform and
-  // ptxas does not turn it into a warp-aggregated atomic, whose result
-  // broadcast (SHFL) would wait for the atomic right away.
+  // Lane 0 alone issues the claim, as inline PTX: the compiler's
+  // warp-aggregated atomicAdd would broadcast the result (SHFL) right away
+  // and so wait for the atomic; here the result stays in lane 0 until the
+  // chunk after next needs it.
   long long next_raw = 0;
-  auto claim = [&]() {
-    unsigned long long* addr = lane == 0 ? a.cursor : a.cursor + 1 + lane;
-    const unsigned long long inc = lane == 0 ? (unsigned long long)kDeepChunk : 0ULL;
-    next_raw = (long long)atomicAdd(addr, inc);
-  };
+  const unsigned lane_op = opaque_u32(lane);
+  auto claim = [&]() { if (lane == 0) next_raw = claim_chunk(a.cursor + lane_op); };
   auto advance = [&](long long x) -> long long {
     if (((x + 1) & (kDeepChunk - 1)) != 0) return x + 1;
     const long long r = __shfl_sync(0xffffffffu, next_raw, 0);
@@ -315,17 +340,43 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
   long long jn = advance(j);
   int c = 0, cn = 0;
   double s_c = 0.0, T_c = 0.0, q_c = 0.0;
+  // NARROW: an entry's (s, T[lane], q[lane]) are staged one column ahead
+  // into this warp's double buffer s_stage[2][3][32] by per-lane cp.async
+  // (each lane copies s into its own slot), so the prefetch holds no
+  // registers and no register scoreboard -- a register prefetch shared its
+  // scoreboard with the column's other loads and stalled them.
+  int buf = 0;
+  const unsigned st_addr = opaque_u32(smem_u32(s_stage + lane));
+  auto stage = [&](int cc, int b) {
+    const unsigned d = st_addr + b * 768;
+    cp_async8_u32(d, a.s + cc);
+    if (lane < L) {
+      cp_async8_u32(d + 256, a.T + (long long)lane * a.ld_in + cc);
+      cp_async8_u32(d + 512, a.q + (long long)lane * a.ld_in + cc);
+    }
+    cp_async_commit();
+  };
   if (j < A) {
     c = a.idx[j];
     if (jn < A) cn = a.idx[jn];
-    s_c = a.s[c];
-    if (NARROW && lane < L) {
-      T_c = a.T[(long long)lane * a.ld_in + c];
-      q_c = a.q[(long long)lane * a.ld_in + c];
-    }
+    if (NARROW) stage(c, 0);
+    else s_c = a.s[c];
   }
   int nb = 0;  // columns parked in the batch
   while (j < A) {
+    if (NARROW) {
+      // before this column's list load: the wait covers every outstanding
+      // load of the thread, so a fresh one would be waited for too
+      cp_async_wait_all();
+      const unsigned d = st_addr + buf * 768;
+      s_c = lds_f64(d);
+      if (lane < L) {
+        T_c = lds_f64(d + 256);
+        q_c = lds_f64(d + 512);
+      }
+      if (jn < A) stage(cn, buf ^ 1);
+      buf ^= 1;
+    }
     const long long jnn = (jn < A) ? advance(jn) : A;
     const int cnn = (jnn < A) ? a.idx[jnn] : 0;
     const double sc = s_c;
@@ -346,11 +397,6 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       if (NARROW) {
         T = T_c;
         q = q_c;
-        if (jn < A) {  // prefetch the next entry behind the solves
-          s_c = a.s[cn];
-          T_c = a.T[(long long)lane * a.ld_in + cn];
-          q_c = a.q[(long long)lane * a.ld_in + cn];
-        }
       } else {
         T = a.T[(long long)k * a.ld_in + c];
         q = a.q[(long long)k * a.ld_in + c];
@@ -562,11 +608,8 @@ __device__ __forceinline__ void deep_worker_pairs(const DeepArgs& a, const doubl
   const int L = a.L;
   const long long A = *a.count;
   long long next_raw = 0;
-  auto claim = [&]() {
-    unsigned long long* addr = lane == 0 ? a.cursor : a.cursor + 1 + lane;
-    const unsigned long long inc = lane == 0 ? (unsigned long long)kDeepChunk : 0ULL;
-    next_raw = (long long)atomicAdd(addr, inc);
-  };
+  const unsigned lane_op = opaque_u32(lane);
+  auto claim = [&]() { if (lane == 0) next_raw = claim_chunk(a.cursor + lane_op); };
   auto advance = [&](long long x) -> long long {   // next pair start
     if (((x + 2) & (kDeepChunk - 1)) != 0) return x + 2;
     const long long r = __shfl_sync(0xffffffffu, next_raw, 0);
@@ -744,8 +787,8 @@ __device__ __forceinline__ void shallow_column_src(const ShallowArgs& a, long lo
   if (DO_DEEP_ZERO && !(sc > a.thr)) {
 #pragma unroll 10
     for (int k = 0; k < L; ++k) {
-      a.d_tend_T[(long long)k * a.d_ld_out + c] = 0.0;
-      a.d_tend_q[(long long)k * a.d_ld_out + c] = 0.0;
+      __stcs(&a.d_tend_T[(long long)k * a.d_ld_out + c], 0.0);
+      __stcs(&a.d_tend_q[(long long)k * a.d_ld_out + c], 0.0);
     }
     a.d_precip[c] = 0.0;
     a.d_work[c] = 0;
@@ -816,8 +859,8 @@ __device__ __forceinline__ void shallow_column_src(const ShallowArgs& a, long lo
   if (!survived) {
 #pragma unroll 10
     for (int k = 0; k < L; ++k) {
-      a.tend_T[(long long)k * a.ld_out + c] = 0.0;
-      a.tend_q[(long long)k * a.ld_out + c] = 0.0;
+      __stcs(&a.tend_T[(long long)k * a.ld_out + c], 0.0);
+      __stcs(&a.tend_q[(long long)k * a.ld_out + c], 0.0);
     }
     a.precip[c] = 0.0;
     a.exited[c] = 1;
@@ -829,8 +872,8 @@ __device__ __forceinline__ void shallow_column_src(const ShallowArgs& a, long lo
   for (int k = 0; k < L; ++k) {
     const double T = src.t(k);
     const double q = src.m(k);
-    a.tend_T[(long long)k * a.ld_out + c] = mul(0.005, sub(base, T));
-    a.tend_q[(long long)k * a.ld_out + c] = mul(0.02, sub(0.012, q));
+    __stcs(&a.tend_T[(long long)k * a.ld_out + c], mul(0.005, sub(base, T)));
+    __stcs(&a.tend_q[(long long)k * a.ld_out + c], mul(0.02, sub(0.012, q)));
   }
   a.precip[c] = mul(sub(sc, 0.5), max0(add(sa, 0.5)));
   a.exited[c] = 0;
@@ -933,11 +976,23 @@ __global__ void __launch_bounds__(kShTile, 1) shallow_tma_kernel(ShallowArgs a) 
 // Persistent deep kernel: one block per SM; every warp works the deep list
 // (deep_worker).  kDeepWarps when it runs alone, kDeepWarpsOverlap when the
 // shallow kernel shares the SMs (convgpu.cu, overlap mode).
-constexpr int kDeepWarps = 24;
-constexpr int kDeepWarpsOverlap = 20;  // leaves an SM's worth of room for shallow blocks
+// Measured (f02, 1 B200): alone, 16 warps beat 20 and 24 (0.585 vs 0.599 ms
+// at 24 -- fewer, unconstrained warps keep their state in registers); in
+// overlap mode 12 warps (~37K registers) leave room for three 128-thread
+// shallow blocks per SM, enough for the shallow kernel to finish under the
+// deep one (step 0.767 ms, against 0.83 at 16 warps and 0.89 at 20).
+constexpr int kDeepWarps = 16;
+constexpr int kDeepWarpsOverlap = 12;
+
+// Register cap per thread: the register file divided over one block of NW
+// warps (the kernel needs ~94, so 12 and 16 warps are unconstrained).
+template <int NW>
+constexpr int deep_max_regs() {
+  return ((65536 / (NW * 32)) & ~7) > 255 ? 255 : ((65536 / (NW * 32)) & ~7);
+}
 
 template <int VAR, bool NARROW, int NW, bool PAIRS = false>
-__global__ void __launch_bounds__(NW * 32, 1) deep_kernel(DeepArgs a) {
+__global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (a.trace && threadIdx.x == 0) {
     a.trace[3 * blockIdx.x] = smid();
@@ -945,6 +1000,7 @@ __global__ void __launch_bounds__(NW * 32, 1) deep_kernel(DeepArgs a) {
   }
   __shared__ int s_bcol[NW][kDeepBatch];
   __shared__ int s_bwork[NW][kDeepBatch];
+  __shared__ __align__(16) double s_stage[NARROW && !PAIRS ? NW : 1][2 * 3 * 32];
   double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
   if (VAR != kVarApprox) {
     for (int i = threadIdx.x; i < kExpTableSize * kTabCopies; i += blockDim.x)
@@ -956,7 +1012,8 @@ __global__ void __launch_bounds__(NW * 32, 1) deep_kernel(DeepArgs a) {
   double* s_term = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies) +
                    (size_t)wib * a.batch * a.L;
   if (PAIRS && NARROW) deep_worker_pairs<VAR>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], lane);
-  else deep_worker<VAR, NARROW>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], lane);
+  else deep_worker<VAR, NARROW>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib],
+                                s_stage[NARROW && !PAIRS ? wib : 0], lane);
   if (a.trace) {
     __syncthreads();
     if (threadIdx.x == 0) a.trace[3 * blockIdx.x + 2] = gtimer();

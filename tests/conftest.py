@@ -29,3 +29,19 @@ def ctx():
     c = P.Context(0)
     yield c
     c.close()
+
+
+def env_context(**env):
+    """A Context created with CVG_* tuning switches set (they are read at
+    context creation), e.g. env_context(CVG_STRICT="1")."""
+    import paper_1711_00289_b200 as P
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return P.Context(0)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v

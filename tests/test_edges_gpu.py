@@ -175,16 +175,8 @@ def test_device_resident_async_path(ctx):
 def small_chunk_ctx():
     """A context whose host-buffer calls pipeline 1000-column chunks, so a
     few thousand columns cross several chunks and reuse every workspace slot."""
-    import os
-    old = os.environ.get("CVG_CHUNK_COLS")
-    os.environ["CVG_CHUNK_COLS"] = "1000"
-    try:
-        c = P.Context(0)
-    finally:
-        if old is None:
-            del os.environ["CVG_CHUNK_COLS"]
-        else:
-            os.environ["CVG_CHUNK_COLS"] = old
+    from conftest import env_context
+    c = env_context(CVG_CHUNK_COLS="1000")
     yield c
     c.close()
 

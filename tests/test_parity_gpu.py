@@ -152,3 +152,45 @@ def test_approx_exp_bit_exact(ctx):
     lib = O.lib()
     want = np.array([lib.orc_approx_exp(float(v)) for v in x])
     assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+@pytest.fixture(scope="module")
+def strict_ctx():
+    """Reference rounding in every Newton update (CVG_STRICT=1), for all
+    variants -- the path the relaxed update of Exact/StrengthReduced
+    replaces by default (colmath.cuh, newton_relaxed_step)."""
+    from conftest import env_context
+    c = env_context(CVG_STRICT="1")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("cfg,kw", [("c1", {}), ("c4", {"shape": (96, 144)})], ids=["c1", "c4"])
+def test_strict_update_matches_oracle_and_relaxed(ctx, strict_ctx, cfg, kw, variant):
+    s, T, q = G.make_config(cfg, seed=13, **kw)
+    o = P.KernelOptions(variant=variant)
+    oo = O.Options(variant=variant)
+    od, osh = O.convection("deep", s, T, q, oo), O.convection("shallow", s, T, q, oo)
+    d_strict, s_strict = strict_ctx.convect(s, T, q, o)
+    d_relax, s_relax = ctx.convect(s, T, q, o)
+    check(d_strict, od, "deep")
+    check(s_strict, osh, "shallow")
+    check(d_relax, od, "deep")
+    # the two device paths differ only by rounding noise: same flags, work
+    # equal outside the Newton-margin class, fp64 fields within tolerance
+    check(d_relax, {"tend_T": d_strict.tend_T, "tend_q": d_strict.tend_q, "precip": d_strict.precip,
+                    "work": d_strict.work_units, "exited": d_strict.exited_early}, "deep", margin=od.margin)
+    for f in ("tend_T", "tend_q", "precip", "work_units", "exited_early"):
+        assert np.array_equal(getattr(s_relax, f), getattr(s_strict, f))   # shallow has no Newton
+
+
+def test_relaxed_guard_falls_back_for_tight_tolerance(ctx, strict_ctx):
+    """newton_tol below 2^-40 * 2^floor(log2 |y|) takes the exact update
+    (relaxed_ok): results equal the strict path bit for bit."""
+    s, T, q = G.make_config("c1", n=512, seed=3)
+    o = P.KernelOptions(newton_tol=2e-13)
+    a, _ = ctx.convect(s, T, q, o)
+    b, _ = strict_ctx.convect(s, T, q, o)
+    for f in ("tend_T", "tend_q", "precip", "work_units", "exited_early"):
+        assert np.array_equal(getattr(a, f), getattr(b, f))
