@@ -205,6 +205,7 @@ template <int VAR, bool NARROW, int NW, bool PAIRS = false>
 void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
   const int threads = NW * 32;
   const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
+                      (size_t)NW * cvg::deep_stage_doubles<NARROW, PAIRS>() * sizeof(double) +
                       (size_t)NW * a.batch * a.L * sizeof(double);
   auto kern = cvg::deep_kernel<VAR, NARROW, NW, PAIRS>;
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -228,7 +229,10 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     // shallow blocks beside the deep block; kDeepWarps when deep runs alone
     const int nw = ctx->deep_warps > 0 ? ctx->deep_warps : (ov ? cvg::kDeepWarpsOverlap : cvg::kDeepWarps);
     if (ctx->pairs && a.L <= 32) {
-      launch_deep_t<VAR, true, 14, true>(ctx, a, st);
+      if (nw == 8) launch_deep_t<VAR, true, 8, true>(ctx, a, st);
+      else if (nw == 10) launch_deep_t<VAR, true, 10, true>(ctx, a, st);
+      else if (nw == 12) launch_deep_t<VAR, true, 12, true>(ctx, a, st);
+      else launch_deep_t<VAR, true, 16, true>(ctx, a, st);
     } else if (a.L <= 32) {
       if (nw == 16) launch_deep_t<VAR, true, 16>(ctx, a, st);
       else if (nw == 20) launch_deep_t<VAR, true, 20>(ctx, a, st);
@@ -252,9 +256,17 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     k<<<ctx->num_sms, cvg::kShTile, smem, st>>>(b);
   } else {
     const unsigned blocks = (unsigned)((b.n + cvg::kShallowThreads - 1) / cvg::kShallowThreads);
-    if (sh && dp) cvg::shallow_kernel<VAR, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
-    else if (sh) cvg::shallow_kernel<VAR, true, false><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
-    else if (dp) cvg::shallow_kernel<VAR, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    const bool relax = VAR != cvg::kVarApprox && !ctx->strict;
+    if (sh && relax) {
+      if (dp) cvg::shallow_kernel<VAR, true, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+      else cvg::shallow_kernel<VAR, true, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    } else if (sh && dp) {
+      cvg::shallow_kernel<VAR, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    } else if (sh) {
+      cvg::shallow_kernel<VAR, true, false><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    } else if (dp) {
+      cvg::shallow_kernel<VAR, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+    }
   }
   CVG_CUDA(cudaGetLastError());
   if (pe) CVG_CUDA(cudaEventRecord(pe[3], st));

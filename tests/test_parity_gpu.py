@@ -177,12 +177,14 @@ def test_strict_update_matches_oracle_and_relaxed(ctx, strict_ctx, cfg, kw, vari
     check(d_strict, od, "deep")
     check(s_strict, osh, "shallow")
     check(d_relax, od, "deep")
+    check(s_relax, osh, "shallow")
     # the two device paths differ only by rounding noise: same flags, work
     # equal outside the Newton-margin class, fp64 fields within tolerance
     check(d_relax, {"tend_T": d_strict.tend_T, "tend_q": d_strict.tend_q, "precip": d_strict.precip,
                     "work": d_strict.work_units, "exited": d_strict.exited_early}, "deep", margin=od.margin)
-    for f in ("tend_T", "tend_q", "precip", "work_units", "exited_early"):
-        assert np.array_equal(getattr(s_relax, f), getattr(s_strict, f))   # shallow has no Newton
+    # strict shallow keeps the reference's per-term phase sums: bit-identical
+    # flags and phase counts, fp64 fields equal to the oracle's roundings
+    assert np.array_equal(s_strict.work_units, osh.work) and np.array_equal(s_strict.exited_early, osh.exited)
 
 
 def test_relaxed_guard_falls_back_for_tight_tolerance(ctx, strict_ctx):
