@@ -100,12 +100,12 @@ struct Workspace {
   cudaStream_t stream = nullptr;  // chunk stream (host-buffer calls)
   cudaStream_t side = nullptr;    // shallow kernel, concurrent with deep
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  DevBuf<int> idx;                     // compacted triggered columns
-  DevBuf<int> counters;                // [0] triggered count
+  DevBuf<long long> groups;            // compacted column groups with a triggered column
+  DevBuf<int> counters;                // [0] listed groups, [1] triggered columns
   DevBuf<unsigned long long> cursor;   // [0] deep work cursor, [1..32] dummies
   DevBuf<unsigned long long> err;      // [0] deep, [1] shallow failure key
   unsigned long long* h_err = nullptr; // pinned mirror of err[0..1]
-  int* h_count = nullptr;              // pinned mirror of counters[0]
+  int* h_count = nullptr;              // pinned mirror of counters[0..1]
   // staging for host-buffer calls (chunk-sized)
   DevBuf<double> in_s, in_T, in_q, dT, dq, dp, sT, sq, sp;
   DevBuf<long long> dw, sw;
@@ -128,7 +128,7 @@ struct Workspace {
   void destroy() {
     for (auto* b : {&in_s, &in_T, &in_q, &dT, &dq, &dp, &sT, &sq, &sp}) b->release();
     dw.release(); sw.release(); dx.release(); sx.release();
-    idx.release(); counters.release(); cursor.release(); err.release();
+    groups.release(); counters.release(); cursor.release(); err.release();
     if (h_err) cudaFreeHost(h_err);
     if (h_count) cudaFreeHost(h_count);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -157,9 +157,10 @@ struct cvg_context {
   unsigned long long* h_aux_err = nullptr;
   // tuning switches (environment, read at context creation)
   bool overlap = true;     // CVG_OVERLAP: deep || shallow on two streams
-  bool pairs = false;      // CVG_PAIRS: two deep columns per warp (ILP 4)
   int shallow_mode = 0;    // CVG_SHALLOW_MODE: 0 thread per column, 2 TMA-staged tiles
   int deep_warps = 0;      // CVG_DEEP_WARPS: 12, 16 or 20 warps per deep block (0: by mode)
+  bool fused = false;      // CVG_FUSED: shallow tiles inside the deep kernel (L <= 32)
+  int shallow_minb = 8;    // CVG_SHALLOW_MINB: shallow blocks per SM the register budget targets (8, 12, 16)
   bool strict = false;     // CVG_STRICT: reference rounding in every Newton update (all variants)
   long long chunk_cols = kChunkCols;  // CVG_CHUNK_COLS: host-call pipeline chunk
   int slots = 3;                      // CVG_SLOTS: workspaces used by host-buffer calls (1..kSlots)
@@ -201,17 +202,19 @@ bool valid_options(const cvg_options* o, std::string* why) {
   return true;
 }
 
-template <int VAR, bool NARROW, int NW, bool PAIRS = false>
-void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
+// Shared memory of one deep block: both exp tables and the per-warp scratch.
+template <int VAR, bool NARROW, int NW, bool FUSED = false, bool SH = true, bool RELAX_SH = false>
+void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st,
+                   const cvg::ShallowArgs& b = cvg::ShallowArgs{}) {
   const int threads = NW * 32;
   const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
-                      (size_t)NW * cvg::deep_stage_doubles<NARROW, PAIRS>() * sizeof(double) +
-                      (size_t)NW * a.batch * a.L * sizeof(double);
-  auto kern = cvg::deep_kernel<VAR, NARROW, NW, PAIRS>;
+                      (size_t)cvg::kExpTableSize * cvg::kTab1Copies * sizeof(double) +
+                      (size_t)NW * cvg::deep_warp_doubles(NARROW, a.L) * sizeof(double);
+  auto kern = cvg::deep_kernel<VAR, NARROW, NW, FUSED, SH, RELAX_SH>;
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // full shared-memory carveout, so a shallow block still fits beside it
+  // full shared-memory carveout, so shallow blocks still fit beside it
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  kern<<<ctx->num_sms, threads, smem, st>>>(a);
+  kern<<<ctx->num_sms, threads, smem, st>>>(a, b);
   CVG_CUDA(cudaGetLastError());
 }
 
@@ -221,6 +224,18 @@ void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
 template <int VAR>
 void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh,
                     bool dp, cudaEvent_t* pe, cudaStream_t st) {
+  if (ctx->fused && dp && a.L <= 32) {
+    // one kernel: deep groups with shallow tiles interleaved
+    const bool relax = VAR != cvg::kVarApprox && !ctx->strict;
+    if (sh && relax) launch_deep_t<VAR, true, 20, true, true, true>(ctx, a, st, b);
+    else if (sh) launch_deep_t<VAR, true, 20, true, true, false>(ctx, a, st, b);
+    else launch_deep_t<VAR, true, 20, true, false, false>(ctx, a, st, b);
+    if (pe) {
+      CVG_CUDA(cudaEventRecord(pe[2], st));
+      CVG_CUDA(cudaEventRecord(pe[3], st));
+    }
+    return;
+  }
   const bool ov = ctx->overlap && dp;
   const cudaStream_t main = st;
   if (ov) CVG_CUDA(cudaEventRecord(w.ev_fork, st));
@@ -228,14 +243,11 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     // deep block size: kDeepWarpsOverlap leaves each SM room for three
     // shallow blocks beside the deep block; kDeepWarps when deep runs alone
     const int nw = ctx->deep_warps > 0 ? ctx->deep_warps : (ov ? cvg::kDeepWarpsOverlap : cvg::kDeepWarps);
-    if (ctx->pairs && a.L <= 32) {
-      if (nw == 8) launch_deep_t<VAR, true, 8, true>(ctx, a, st);
-      else if (nw == 10) launch_deep_t<VAR, true, 10, true>(ctx, a, st);
-      else if (nw == 12) launch_deep_t<VAR, true, 12, true>(ctx, a, st);
-      else launch_deep_t<VAR, true, 16, true>(ctx, a, st);
-    } else if (a.L <= 32) {
+    if (false) {    } else if (a.L <= 32) {
       if (nw == 16) launch_deep_t<VAR, true, 16>(ctx, a, st);
       else if (nw == 20) launch_deep_t<VAR, true, 20>(ctx, a, st);
+      else if (nw == 14) launch_deep_t<VAR, true, 14>(ctx, a, st);
+      else if (nw == 24) launch_deep_t<VAR, true, 24>(ctx, a, st);
       else launch_deep_t<VAR, true, 12>(ctx, a, st);
     } else {
       if (nw == 16) launch_deep_t<VAR, false, 16>(ctx, a, st);
@@ -258,7 +270,9 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     const unsigned blocks = (unsigned)((b.n + cvg::kShallowThreads - 1) / cvg::kShallowThreads);
     const bool relax = VAR != cvg::kVarApprox && !ctx->strict;
     if (sh && relax) {
-      if (dp) cvg::shallow_kernel<VAR, true, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+      if (dp && ctx->shallow_minb == 12) cvg::shallow_kernel<VAR, true, true, true, 12><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+      else if (dp && ctx->shallow_minb == 16) cvg::shallow_kernel<VAR, true, true, true, 16><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+      else if (dp) cvg::shallow_kernel<VAR, true, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
       else cvg::shallow_kernel<VAR, true, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
     } else if (sh && dp) {
       cvg::shallow_kernel<VAR, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
@@ -285,26 +299,26 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
   const long long n = in->n_columns;
   const int L = in->n_levels;
   CVG_CUDA(cudaMemsetAsync(w.counters.p, 0, 4 * sizeof(int), st));
-  CVG_CUDA(cudaMemsetAsync(w.cursor.p, 0, sizeof(unsigned long long), st));
+  CVG_CUDA(cudaMemsetAsync(w.cursor.p, 0, 17 * sizeof(unsigned long long), st));
   CVG_CUDA(cudaMemsetAsync(w.err.p, 0xff, 2 * sizeof(unsigned long long), st));
   if (n == 0) return;
   const bool do_deep = (mask & CVG_DEEP) != 0, do_sh = (mask & CVG_SHALLOW) != 0;
   if (pe) CVG_CUDA(cudaEventRecord(pe[0], st));
   cvg::DeepArgs a{};
   if (do_deep) {
-    w.idx.ensure((size_t)n);
-    const unsigned tb = (unsigned)((n + cvg::kTrigTile - 1) / cvg::kTrigTile);
-    cvg::trigger_compact_kernel<<<tb, cvg::kTrigThreads, 0, st>>>(in->s, n, o->activity_threshold, w.idx.p,
-                                                                   w.counters.p, w.err.p);
+    const long long ngroups = (n + cvg::kGroupCols - 1) / cvg::kGroupCols;
+    w.groups.ensure((size_t)ngroups);
+    const unsigned tb = (unsigned)((ngroups + cvg::kTrigThreads - 1) / cvg::kTrigThreads);
+    cvg::trigger_groups_kernel<<<tb, cvg::kTrigThreads, 0, st>>>(in->s, n, o->activity_threshold, in->first_col,
+                                                                  w.groups.p, w.counters.p, w.err.p);
     CVG_CUDA(cudaGetLastError());
     a.s = in->s; a.T = in->T; a.q = in->q; a.ld_in = in->ld;
     a.tend_T = deep->tend_T; a.tend_q = deep->tend_q; a.precip = deep->precip;
     a.work = deep->work_units; a.exited = deep->exited_early; a.ld_out = deep->ld;
-    a.idx = w.idx.p; a.count = w.counters.p; a.cursor = w.cursor.p;
+    a.groups = w.groups.p; a.count = w.counters.p; a.cursor = w.cursor.p; a.n = n;
     a.err = w.err.p; a.first_col = in->first_col;
     a.thr = o->activity_threshold; a.tol = o->newton_tol; a.maxit = o->newton_max_iter;
     a.L = L;
-    a.batch = std::max(1, std::min(cvg::kDeepBatch, (int)(98304 / ((size_t)cvg::kDeepWarps * L * sizeof(double)))));
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
     a.relaxed = !ctx->strict;
   }
@@ -340,7 +354,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
 // Queues the D2H of a workspace's latched failure words / trigger count.
 void read_flags_async(Workspace& w, cudaStream_t st) {
   CVG_CUDA(cudaMemcpyAsync(w.h_err, w.err.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  CVG_CUDA(cudaMemcpyAsync(w.h_count, w.counters.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CVG_CUDA(cudaMemcpyAsync(w.h_count, w.counters.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
 }
 
 // Turns the folded failure keys (minimum over the call's chunks) into the
@@ -445,8 +459,9 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
     if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
-    if (const char* e = getenv("CVG_PAIRS")) ctx->pairs = atoi(e) != 0;
     if (const char* e = getenv("CVG_STRICT")) ctx->strict = atoi(e) != 0;
+    if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
+    if (const char* e = getenv("CVG_FUSED")) ctx->fused = atoi(e) != 0;
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
     if (const char* e = getenv("CVG_SHALLOW_MODE")) ctx->shallow_mode = atoi(e);
     if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
@@ -540,7 +555,7 @@ cvg_status cvg_convect_check(cvg_context* ctx, void* stream, cvg_stats* stats) {
         fclose(f);
       }
     }
-    return collect(&w.h_err[0], &w.h_err[1], *w.h_count, ctx->last_mask, ctx->last_maxit, ctx->last_n, stats);
+    return collect(&w.h_err[0], &w.h_err[1], w.h_count[1], ctx->last_mask, ctx->last_maxit, ctx->last_n, stats);
   });
 }
 
@@ -590,7 +605,7 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
       CVG_CUDA(cudaStreamSynchronize(w.stream));
       md = std::min(md, w.h_err[0]);
       ms_ = std::min(ms_, w.h_err[1]);
-      trig += *w.h_count;
+      trig += w.h_count[1];
     };
     for (long long ci = 0; ci < nchunks; ++ci) {
       const int slot = (int)(ci % ctx->slots);

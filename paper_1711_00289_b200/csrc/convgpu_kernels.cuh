@@ -45,84 +45,64 @@ __device__ __forceinline__ void raise_failure(unsigned long long* err, long long
 __device__ __forceinline__ double max0(double x) { return (0.0 < x) ? x : 0.0; }
 
 // ---------------------------------------------------------------------------
-// Trigger + stream compaction.  Each 1024-thread block owns a tile of 4096
-// consecutive columns (4 per thread, coalesced).  A triggered column's Newton
-// work is set almost entirely by its guess 24 + 160 s (physics.cpp:121;
-// iteration count is monotone in the guess, physics.hpp:103-107), so the
-// tile's triggered columns are written bucketed by s (kTrigBuckets buckets
-// over (thr, 1]), column order inside a bucket: warps of the deep kernel then
-// hold columns of near-equal work.  __match_any_sync ranks lanes within a
-// (bucket, warp) group, a block scan over (bucket, slot, warp) counts gives
-// the offsets, and one atomicAdd per block reserves the tile's slice.
-constexpr int kTrigThreads = 1024;
-constexpr int kTrigPerThread = 4;
-constexpr int kTrigTile = kTrigThreads * kTrigPerThread;
-constexpr int kTrigBuckets = 16;
+// Trigger + stream compaction into column GROUPS.  A group is 4 consecutive
+// columns -- one 32-byte sector of every level row -- and the list holds
+// each group with at least one triggered column as (group << 4) | mask.  The
+// deep kernel works through a group's triggered columns and writes the
+// group's deep outputs as whole sectors (zeros for its untriggered
+// columns); the shallow kernel zero-fills only groups without a triggered
+// column.  Per-column 8-byte stores of the deep outputs were partial-sector
+// writes (read-modify-write in L2/DRAM) and bounded the deep kernel.
+// One thread per group (4 coalesced loads of s), warp ballot + block scan,
+// one atomicAdd per block reserves the block's slice; counts[0] = groups,
+// counts[1] = triggered columns.
+constexpr int kTrigThreads = 256;
+constexpr int kGroupCols = 4;
 
 __global__ void __launch_bounds__(kTrigThreads)
-trigger_compact_kernel(const double* __restrict__ s, long long n, double thr,
-                       int* __restrict__ idx, int* __restrict__ count,
-                       unsigned long long* __restrict__ err_deep) {
-  constexpr int kSlots = kTrigBuckets * kTrigPerThread * 32;  // (bucket, i, warp)
-  __shared__ int s_cnt[kSlots];
-  __shared__ int s_wsum[32];
+trigger_groups_kernel(const double* __restrict__ s, long long n, double thr, long long first_col,
+                      long long* __restrict__ groups, int* __restrict__ counts,
+                      unsigned long long* __restrict__ err_deep) {
+  constexpr int kWarps = kTrigThreads / 32;
+  __shared__ int s_wsum[kWarps];
+  __shared__ int s_cols[kWarps];
   __shared__ int s_base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long tile0 = (long long)blockIdx.x * kTrigTile;
-  for (int i = threadIdx.x; i < kSlots; i += kTrigThreads) s_cnt[i] = 0;
-  __syncthreads();
-  const double scale = kTrigBuckets / fmax(1.0 - thr, 1e-300);
-  int bkt[kTrigPerThread];
-  unsigned same[kTrigPerThread];
+  const long long g = (long long)blockIdx.x * kTrigThreads + threadIdx.x;
+  unsigned m = 0;
 #pragma unroll
-  for (int i = 0; i < kTrigPerThread; ++i) {
-    const long long c = tile0 + (long long)i * kTrigThreads + threadIdx.x;
-    int b = -1;
+  for (int i = 0; i < kGroupCols; ++i) {
+    const long long c = g * kGroupCols + i;
     if (c < n) {
       const double sc = s[c];
-      if (!is_finite(sc)) raise_failure(err_deep, c, 0, kFailActivity);
-      if (sc > thr) b = min(kTrigBuckets - 1, max(0, (int)((sc - thr) * scale)));
+      if (!is_finite(sc)) raise_failure(err_deep, first_col + c, 0, kFailActivity);
+      if (sc > thr) m |= 1u << i;
     }
-    bkt[i] = b;
-    same[i] = __match_any_sync(0xffffffffu, b);
-    if (b >= 0 && lane == __ffs(same[i]) - 1) s_cnt[(b * kTrigPerThread + i) * 32 + warp] = __popc(same[i]);
   }
-  __syncthreads();
-  // block-wide exclusive scan of the kSlots counts (2 per thread)
-  const int e0 = 2 * threadIdx.x;
-  const int v0 = s_cnt[e0], v1 = s_cnt[e0 + 1];
-  int incl = v0 + v1;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
+  const unsigned bal = __ballot_sync(0xffffffffu, m != 0);
+  const int ncols = __reduce_add_sync(0xffffffffu, __popc(m));
+  if (lane == 0) {
+    s_wsum[warp] = __popc(bal);
+    s_cols[warp] = ncols;
   }
-  if (lane == 31) s_wsum[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    const int w = s_wsum[lane];
-    int wi = w;
+    const int v = lane < kWarps ? s_wsum[lane] : 0;
+    int incl = v;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += t;
+    for (int o = 1; o < kWarps; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
     }
-    s_wsum[lane] = wi - w;
-    if (lane == 31) s_base = wi > 0 ? atomicAdd(count, wi) : 0;
-  }
-  __syncthreads();
-  const int excl = s_wsum[warp] + incl - (v0 + v1);
-  s_cnt[e0] = excl;
-  s_cnt[e0 + 1] = excl + v0;
-  __syncthreads();
-  const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int i = 0; i < kTrigPerThread; ++i) {
-    if (bkt[i] >= 0) {
-      const long long c = tile0 + (long long)i * kTrigThreads + threadIdx.x;
-      idx[s_base + s_cnt[(bkt[i] * kTrigPerThread + i) * 32 + warp] + __popc(same[i] & lt)] = (int)c;
+    const int cols = __reduce_add_sync(0xffffffffu, lane < kWarps ? s_cols[lane] : 0);
+    if (lane < kWarps) s_wsum[lane] = incl - v;
+    if (lane == kWarps - 1) {
+      s_base = incl > 0 ? atomicAdd(&counts[0], incl) : 0;
+      if (cols > 0) atomicAdd(&counts[1], cols);
     }
   }
+  __syncthreads();
+  if (m) groups[s_base + s_wsum[warp] + __popc(bal & ((1u << lane) - 1u))] = (g << 4) | (long long)m;
 }
 
 // ---------------------------------------------------------------------------
@@ -138,9 +118,10 @@ struct DeepArgs {
   long long* work;
   uint8_t* exited;
   long long ld_out;
-  const int* idx;         // compacted triggered columns
+  const long long* groups;  // compacted groups with a triggered column: (group << 4) | mask
   unsigned long long* trace;  // optional [grid][3]: smid, start, end (globaltimer ns)
-  const int* count;       // number of triggered columns (device)
+  const int* count;       // number of listed groups (device)
+  long long n;            // columns
   unsigned long long* cursor;  // [0] work cursor (zeroed per call), [1..32] dummies
   unsigned long long* err;
   const double2* exp_tab; // 2^(j/512) double-double table (global)
@@ -148,14 +129,13 @@ struct DeepArgs {
   double thr, tol;
   int maxit;
   int L;                  // levels
-  int batch;              // columns per precip batch (<= kDeepBatch)
   bool fast_div_ok;       // newton_tol >= 2^-500
   bool relaxed;           // relaxed-rounding Newton update allowed (colmath.cuh)
 };
 
 // Deep-kernel lanes read a lane-private copy of the exp table (see
 // exp_tang); other kernels pass the plain table with kTabCopies = 1 views.
-constexpr int kTabCopies = 8;
+constexpr int kTabCopies = 1;
 
 template <int VAR, int STRIDE = kTabCopies>
 __device__ __forceinline__ double deep_exp(double x, const double2* tab) {
@@ -226,7 +206,8 @@ __device__ __forceinline__ bool newton_finish(const DeepArgs& a, const double2* 
 // (the reference reports the first failure in its own solve order,
 // recovered from the failure key).
 template <int VAR>
-__device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2* tab, long long col,
+__device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2* tab, unsigned tab1_addr,
+                                               long long col,
                                                int k, double ye, double yp, double guess, double e0,
                                                double c0, double& re, double& rp, int& work) {
   const double kBig = 0x1.0p490;
@@ -241,16 +222,12 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
     // noise only; the exact sequence below is the one the reference runs
     const double tol = a.tol;
     const int maxit = a.maxit;
-    // opaque to the compiler, so the lane's table address stays in a
-    // register instead of being rematerialised from %tid inside the loop
-    unsigned tab_addr;
-    asm volatile("mov.b32 %0, %1;" : "=r"(tab_addr) : "r"((unsigned)__cvta_generic_to_shared(tab)));
     int left = maxit + 1;   // updates still allowed (the loop may take one
                             // more than maxit; newton_finish then fails it)
     if (left > 0) do {
       if (abs_le_either(he, hp, tol)) break;
-      newton_relaxed_step<kTabCopies>(te, ee, he, ye, tab_addr);
-      newton_relaxed_step<kTabCopies>(tp, ep, hp, yp, tab_addr);
+      newton_relaxed_step(te, ee, he, ye, tab1_addr);
+      newton_relaxed_step(tp, ep, hp, yp, tab1_addr);
     } while (--left != 0);
     it = maxit + 1 - max(left, 0);
   } else if (fast_ok) {
@@ -292,8 +269,7 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
 // precipitation terms are parked in shared memory and, every kBatch
 // columns, lane i sums column i's terms in k order (physics.cpp:161) -- one
 // warp instruction serves kBatch columns instead of one.
-constexpr int kDeepBatch = 16;
-constexpr int kDeepChunk = 4;   // list entries claimed per atomic (power of 2)
+constexpr int kDeepChunk = 1;   // list entries (groups) claimed per atomic (power of 2)
 
 // Issued by lane 0 only, at cursor + lane (= cursor): an address ptxas
 // cannot prove warp-uniform, so it does not rewrite the atomic into its
@@ -305,26 +281,46 @@ __device__ __forceinline__ long long claim_chunk(unsigned long long* cursor_plus
   return (long long)r;
 }
 
-// The deep role of a warp: walks the compacted list until it is exhausted.
-// s_tab points at this lane's copy of the replicated exp table; s_term is
-// this warp's [batch][L] precip scratch, s_bcol / s_bwork its batch slots.
-template <int VAR, bool NARROW>
-__device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_tab, double* s_term,
-                                            int* s_bcol, int* s_bwork, double* s_stage, int lane) {
+// The group's per-column scalars live in s_gwork / s_gok / s_gpr [4].
+// Per-warp shared scratch of the deep worker, in doubles:
+//   NARROW: staging [2][3][32] (s, T[lane], q[lane] of the next column),
+//           group outputs tend_T, tend_q [4][32] each, precip terms [4][32]
+//   wide:   precip terms [L] of the current column
+__host__ __device__ constexpr int deep_warp_doubles(bool narrow, int L) {
+  return narrow ? 2 * 3 * 32 + 3 * kGroupCols * 32 : L;
+}
+
+// The deep role of a warp: walks the group list until it is exhausted.
+// s_tab points at this lane's copy of the replicated exp table; s_warp is
+// this warp's scratch (deep_warp_doubles), s_gwork / s_gok the group's
+// per-column work counts and success flags.
+// Fused mode (FUSED): between groups the warp also works through 32-column
+// tiles of the shallow scheme (+ deep zero-fill), claimed from a second
+// cursor -- one tile every `every` groups, the rest after the deep list is
+// exhausted -- so the HBM-bound shallow work runs inside the FP64-bound deep
+// kernel's latency shadow instead of competing for SM slots as a second
+// kernel.  tile(t) processes tile t (returns false when t is past the end).
+struct NoTiles {
+  __device__ bool operator()(long long) const { return false; }
+};
+
+template <int VAR, bool NARROW, bool FUSED = false, class Tile = NoTiles>
+__device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_tab, unsigned tab1_addr,
+                                            double* s_warp, int* s_gwork, int* s_gok, double* s_gpr,
+                                            int lane, const Tile& tile = Tile(),
+                                            unsigned long long* tile_cursor = nullptr, int every = 1) {
   const int L = a.L;
-  const long long A = *a.count;
+  const long long G = *a.count;
   const bool reduced = (VAR == kVarReduced);
-  // Work distribution: warps claim aligned chunks of kDeepChunk list
-  // entries from a global cursor (one atomic per chunk), so SMs finish
-  // together whatever the per-column cost mix (cluster intensity varies
-  // across the grid).  Two-deep software pipeline: an entry's (s, T[lane],
-  // q[lane]) are loaded during the previous entry's solves, the entry after
-  // next is known a column ahead, and the next chunk is claimed a chunk
-  // ahead, so no load or atomic sits on the issue path of a column.
+  // Work distribution: warps claim groups from a global cursor (one atomic
+  // per group, a group ahead), so SMs finish together whatever the
+  // per-column cost mix.  Software pipeline: a column's (s, T[lane],
+  // q[lane]) are staged during the previous column's solves, the next
+  // group's entry is known a group ahead, the one after it is loaded then.
   // Lane 0 alone issues the claim, as inline PTX: the compiler's
   // warp-aggregated atomicAdd would broadcast the result (SHFL) right away
   // and so wait for the atomic; here the result stays in lane 0 until the
-  // chunk after next needs it.
+  // group after next needs it.
   long long next_raw = 0;
   const unsigned lane_op = opaque_u32(lane);
   auto claim = [&]() { if (lane == 0) next_raw = claim_chunk(a.cursor + lane_op); };
@@ -334,20 +330,37 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     claim();
     return r;
   };
+  // fused shallow tiles: the next tile index is claimed a tile ahead
+  long long tile_raw = 0;
+  auto tile_claim = [&]() { if (FUSED && lane == 0) tile_raw = claim_chunk(tile_cursor + lane_op); };
+  auto do_tile = [&]() -> bool {
+    const long long tt = __shfl_sync(0xffffffffu, tile_raw, 0);
+    tile_claim();
+    return tile(tt);
+  };
+  tile_claim();
+  auto entry = [&](long long x) -> long long { return x < G ? a.groups[x] : -1; };
   claim();
   long long j = __shfl_sync(0xffffffffu, next_raw, 0);
   claim();
   long long jn = advance(j);
-  int c = 0, cn = 0;
-  double s_c = 0.0, T_c = 0.0, q_c = 0.0;
-  // NARROW: an entry's (s, T[lane], q[lane]) are staged one column ahead
-  // into this warp's double buffer s_stage[2][3][32] by per-lane cp.async
-  // (each lane copies s into its own slot), so the prefetch holds no
-  // registers and no register scoreboard -- a register prefetch shared its
-  // scoreboard with the column's other loads and stalled them.
+  long long e = entry(j), en = entry(jn);
+  long long jnn = jn < G ? advance(jn) : G;
+  long long enn = entry(jnn);
+  int groups_done = 0;
+  if (e < 0) {
+    if (FUSED) while (do_tile()) {}
+    return;
+  }
+  double* s_outT = s_warp + 2 * 3 * 32;   // NARROW: [4][32]
+  double* s_outQ = s_outT + kGroupCols * 32;
+  double* s_term = NARROW ? s_outQ + kGroupCols * 32 : s_warp;   // NARROW: [4][32]; wide: [L]
+  // NARROW: per-lane cp.async staging of the next column into a double
+  // buffer (each lane copies s into its own slot) -- no registers, no
+  // register scoreboard shared with the column's other loads
   int buf = 0;
-  const unsigned st_addr = opaque_u32(smem_u32(s_stage + lane));
-  auto stage = [&](int cc, int b) {
+  const unsigned st_addr = opaque_u32(smem_u32(s_warp + lane));
+  auto stage = [&](long long cc, int b) {
     const unsigned d = st_addr + b * 768;
     cp_async8_u32(d, a.s + cc);
     if (lane < L) {
@@ -356,30 +369,31 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     }
     cp_async_commit();
   };
-  if (j < A) {
-    c = a.idx[j];
-    if (jn < A) cn = a.idx[jn];
-    if (NARROW) stage(c, 0);
-    else s_c = a.s[c];
-  }
-  int nb = 0;  // columns parked in the batch
-  while (j < A) {
+  long long g = e >> 4;
+  unsigned m = (unsigned)(e & 15), rem = m;
+  int i = __ffs(rem) - 1;
+  rem &= rem - 1;
+  long long c = g * kGroupCols + i;
+  if (NARROW) stage(c, 0);
+  for (;;) {
+    // the column after this one: the group's next, or the next group's first
+    long long cn = -1;
+    if (rem) cn = g * kGroupCols + (__ffs(rem) - 1);
+    else if (en >= 0) cn = (en >> 4) * kGroupCols + (__ffs((unsigned)(en & 15)) - 1);
+    double sc, T_c = 0.0, q_c = 0.0;
     if (NARROW) {
-      // before this column's list load: the wait covers every outstanding
-      // load of the thread, so a fresh one would be waited for too
       cp_async_wait_all();
       const unsigned d = st_addr + buf * 768;
-      s_c = lds_f64(d);
+      sc = lds_f64(d);
       if (lane < L) {
         T_c = lds_f64(d + 256);
         q_c = lds_f64(d + 512);
       }
-      if (jn < A) stage(cn, buf ^ 1);
+      if (cn >= 0) stage(cn, buf ^ 1);
       buf ^= 1;
+    } else {
+      sc = a.s[c];
     }
-    const long long jnn = (jn < A) ? advance(jn) : A;
-    const int cnn = (jnn < A) ? a.idx[jnn] : 0;
-    const double sc = s_c;
     // physics.cpp:121 / :127 / :146
     const double guess = add(24.0, mul(160.0, sc));
     const double rho = add(1.0, mul(kMC.c005, sc));
@@ -388,10 +402,8 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     const long long col = a.first_col + c;
     int wl = 0;
     bool ok_all = true;
-    // NARROW (L <= 32): one level per lane, its (T, q) prefetched; wide
-    // columns loop over levels lane, lane + 32, ... with plain loads (kept in
-    // a separate instantiation: a conditional load sharing a scoreboard slot
-    // with the prefetch would stall every column on the prefetch)
+    // NARROW (L <= 32): one level per lane, its (T, q) staged; wide columns
+    // loop over levels lane, lane + 32, ... with plain loads
     for (int k = lane; k < L; k += 32) {
       double T, q;
       if (NARROW) {
@@ -400,339 +412,125 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       } else {
         T = a.T[(long long)k * a.ld_in + c];
         q = a.q[(long long)k * a.ld_in + c];
-        if (k == lane && jn < A) s_c = a.s[cn];
       }
-      double m;  // physics.hpp:94-96 via the shared-divisor form of div_rn
+      double m_;  // physics.hpp:94-96 via the shared-divisor form of div_rn
       {
         const double dv = reduced ? mul(rho, rho) : rho;
         if (div_operand_ok(dv) && div_operand_ok(q)) {
           const double ydv = rcp_refined(dv);
-          m = div_by(q, dv, ydv);
-          if (!reduced) m = div_operand_ok(m) ? div_by(m, dv, ydv) : div_rn(m, dv);
+          m_ = div_by(q, dv, ydv);
+          if (!reduced) m_ = div_operand_ok(m_) ? div_by(m_, dv, ydv) : div_rn(m_, dv);
         } else {
-          m = reduced ? div_rn(q, dv) : div_rn(div_rn(q, rho), rho);
+          m_ = reduced ? div_rn(q, dv) : div_rn(div_rn(q, rho), rho);
         }
       }
       // physics.cpp:147-148 / :156-157
-      const double ye = add(add(1.0, mul(1.0e-3, T)), mul(0.1, m));
-      const double yp = add(add(add(1.0, mul(8.0e-4, T)), mul(kMC.c005, m)), mul(0.1, sc));
+      const double ye = add(add(1.0, mul(1.0e-3, T)), mul(0.1, m_));
+      const double yp = add(add(add(1.0, mul(8.0e-4, T)), mul(kMC.c005, m_)), mul(0.1, sc));
       double re = 0.0, rp = 0.0;
       int w = 0;
-      double term = 0.0;
-      if (deep_lane_pair<VAR>(a, s_tab, col, k, ye, yp, guess, e0, c0, re, rp, w)) {
+      double term = 0.0, tT = 0.0, tq = 0.0;
+      if (deep_lane_pair<VAR>(a, s_tab, tab1_addr, col, k, ye, yp, guess, e0, c0, re, rp, w)) {
         // physics.cpp:151-152 / :159-161
         double sin_a, sin_b;
         sin2_cw(add(mul(6.0, T), mul(50.0, q)), mul(3.0, rp), sin_a, sin_b);
-        const long long o = (long long)k * a.ld_out + c;
-        a.tend_T[o] = add(mul(0.02, sub(add(250.0, mul(2.0, re)), T)), mul(0.3, sin_a));
-        a.tend_q[o] = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, sin_b)), q));
+        tT = add(mul(0.02, sub(add(250.0, mul(2.0, re)), T)), mul(0.3, sin_a));
+        tq = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, sin_b)), q));
         term = mul(q, max0(sub(rp, 4.5)));
       } else {
         ok_all = false;
       }
-      s_term[nb * L + k] = term;
+      if (NARROW) {
+        s_outT[i * 32 + k] = tT;
+        s_outQ[i * 32 + k] = tq;
+        s_term[i * 32 + k] = term;
+      } else {
+        a.tend_T[(long long)k * a.ld_out + c] = tT;
+        a.tend_q[(long long)k * a.ld_out + c] = tq;
+        s_term[k] = term;
+      }
       wl += w;
     }
     const int wsum = __reduce_add_sync(0xffffffffu, wl);
     const bool ok = __all_sync(0xffffffffu, ok_all);
     if (lane == 0) {
-      s_bcol[nb] = ok ? c : -1;
-      s_bwork[nb] = wsum;
+      s_gwork[i] = wsum;
+      s_gok[i] = ok;
     }
-    ++nb;
-    c = cn;
-    cn = cnn;
-    j = jn;
-    jn = jnn;
-    if (nb == a.batch || j >= A) {
-      __syncwarp();
-      if (lane < nb) {
-        const int cc = s_bcol[lane];
-        if (cc >= 0) {
-          double pr = 0.0;  // ordered k sum, physics.cpp:161
-          const double* t = s_term + lane * L;
-          for (int kk = 0; kk < L; ++kk) pr = add(pr, t[kk]);
-          a.precip[cc] = pr;
-          a.work[cc] = s_bwork[lane];
-          a.exited[cc] = 0;
+    __syncwarp();
+    if (!NARROW && lane == 0) {   // ordered k sum, physics.cpp:161
+      double pr = 0.0;
+      for (int kk = 0; kk < L; ++kk) pr = add(pr, s_term[kk]);
+      s_gpr[i] = pr;
+    }
+    if (!NARROW) __syncwarp();   // s_term is reused by the next column
+    if (rem == 0) {
+      // last triggered column of group g: write the group's deep outputs,
+      // zeros for its untriggered columns (physics.cpp:89-97)
+      const long long c0g = g * kGroupCols;
+      if (NARROW) {
+        for (int r = lane; r < kGroupCols * L; r += 32) {
+          const int k = r / kGroupCols, ii = r % kGroupCols;
+          const long long cc = c0g + ii;
+          if (cc < a.n) {
+            const bool trig = (m >> ii) & 1u;
+            a.tend_T[(long long)k * a.ld_out + cc] = trig ? s_outT[ii * 32 + k] : 0.0;
+            a.tend_q[(long long)k * a.ld_out + cc] = trig ? s_outQ[ii * 32 + k] : 0.0;
+          }
+        }
+      } else {
+        for (int r = lane; r < kGroupCols * L; r += 32) {
+          const int k = r / kGroupCols, ii = r % kGroupCols;
+          const long long cc = c0g + ii;
+          if (cc < a.n && !((m >> ii) & 1u)) {
+            a.tend_T[(long long)k * a.ld_out + cc] = 0.0;
+            a.tend_q[(long long)k * a.ld_out + cc] = 0.0;
+          }
+        }
+      }
+      if (lane < kGroupCols && c0g + lane < a.n) {
+        const long long cc = c0g + lane;
+        if ((m >> lane) & 1u) {
+          double pr = 0.0;
+          if (NARROW) {   // ordered k sum, physics.cpp:161
+            const double* tt = s_term + lane * 32;
+            for (int kk = 0; kk < L; ++kk) pr = add(pr, tt[kk]);
+          } else {
+            pr = s_gpr[lane];
+          }
+          if (s_gok[lane]) {
+            a.precip[cc] = pr;
+            a.work[cc] = s_gwork[lane];
+            a.exited[cc] = 0;
+          }
+        } else {
+          a.precip[cc] = 0.0;
+          a.work[cc] = 0;
+          a.exited[cc] = 1;
         }
       }
       __syncwarp();
-      nb = 0;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Lockstep Newton over NS independent solves of one lane (physics.cpp:
-// 64-87 each).  Every iteration tests each solve and records its FIRST
-// convergence (root, update count); all NS solves are then updated
-// unconditionally -- a converged solve keeps taking (harmless, in-domain)
-// Newton steps whose results are never used -- so the loop body is
-// straight-line FP64 with NS independent dependency chains.  Solves that
-// enter with their bit set in `done` (fast-path precondition failed) ride
-// along unused; the caller restarts them from the guess with
-// newton_generic, and finishes solves still unconverged after max_iter
-// updates the same way from their state.  RELAX: the relaxed update of
-// colmath.cuh (caller checked relaxed_ok for every solve).
-template <int VAR, int NS, bool RELAX>
-__device__ __forceinline__ void newton_lockstep(const double2* tab, unsigned tab_addr, double tol, int maxit,
-                                                double* t, double* e, double* h, const double* y, double* root,
-                                                int* cnt, unsigned& done) {
-  const unsigned all = (1u << NS) - 1u;
-  int it = 0;
-  for (;;) {
-    // convergence bits of all solves (integer compares, no FP64 pipe); the
-    // record branch is taken about once per solve
-    unsigned conv = 0;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) conv |= (unsigned)abs_le(h[s], tol) << s;
-    const unsigned fresh = conv & ~done;
-    if (fresh) {
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (fresh & (1u << s)) {
-          root[s] = t[s];
-          cnt[s] = it;
-        }
+      if (FUSED && ++groups_done >= every) {
+        groups_done = 0;
+        do_tile();
       }
-      done |= fresh;
+      if (en < 0) break;
+      // next group; load the entry after it
+      e = en;
+      en = enn;
+      j = jn;
+      jn = jnn;
+      jnn = jn < G ? advance(jn) : G;
+      enn = entry(jnn);
+      g = e >> 4;
+      m = (unsigned)(e & 15);
+      rem = m;
     }
-    if (done == all || it >= maxit) break;
-    if (RELAX) {
-#pragma unroll
-      for (int s = 0; s < NS; ++s) newton_relaxed_step<kTabCopies>(t[s], e[s], h[s], y[s], tab_addr);
-    } else {
-#pragma unroll
-      for (int s = 0; s < NS; ++s) t[s] = sub(t[s], div_fast(h[s], add(mul(kMC.c005, e[s]), kMC.c001)));
-#pragma unroll
-      for (int s = 0; s < NS; ++s) e[s] = deep_exp005_fast<VAR>(t[s], tab);
-#pragma unroll
-      for (int s = 0; s < NS; ++s) h[s] = sub(add(e[s], mul(kMC.c001, t[s])), y[s]);
-    }
-    ++it;
+    i = __ffs(rem) - 1;
+    rem &= rem - 1;
+    c = g * kGroupCols + i;
   }
-  // unconverged solves leave with their state after `it` updates
-#pragma unroll
-  for (int s = 0; s < NS; ++s)
-    if (!(done & (1u << s))) cnt[s] = it;
-}
-
-// Per-lane state of one (column, level): inputs, the two solves' results.
-struct LevelSolve {
-  double T, q, ye, yp, re, rp;
-  int work;
-  bool ok;
-};
-
-// Two columns per warp: lane k owns level k of column A and of column B,
-// i.e. FOUR solves in lockstep (entrainment and precipitation of both): four
-// independent dependency chains per lane instead of two.  Consecutive list
-// entries sit in the same s-bucket, so the two columns' iteration counts
-// agree to within about one update.  L <= 32.
-template <int VAR>
-__device__ __forceinline__ void deep_pair_solve(const DeepArgs& a, const double2* tab, unsigned tab_addr,
-                                                int lane, const long long colA, const long long colB,
-                                                double sA, double sB, LevelSolve& A, LevelSolve& B) {
-  const bool reduced = (VAR == kVarReduced);
-  const double kBig = 0x1.0p490;
-  const int k = lane;
-  double guess[2], e0[2], c0[2];
-  LevelSolve* X[2] = {&A, &B};
-  const double sv[2] = {sA, sB};
-#pragma unroll
-  for (int p = 0; p < 2; ++p) {
-    const double sc = sv[p];
-    LevelSolve& Z = *X[p];
-    guess[p] = add(24.0, mul(160.0, sc));                       // physics.cpp:121
-    const double rho = add(1.0, mul(kMC.c005, sc));             // :127 / :146
-    e0[p] = deep_exp<VAR>(mul(kMC.c005, guess[p]), tab);
-    c0[p] = add(e0[p], mul(kMC.c001, guess[p]));
-    double m;  // physics.hpp:94-96 via the shared-divisor form of div_rn
-    const double dv = reduced ? mul(rho, rho) : rho;
-    if (div_operand_ok(dv) && div_operand_ok(Z.q)) {
-      const double ydv = rcp_refined(dv);
-      m = div_by(Z.q, dv, ydv);
-      if (!reduced) m = div_operand_ok(m) ? div_by(m, dv, ydv) : div_rn(m, dv);
-    } else {
-      m = reduced ? div_rn(Z.q, dv) : div_rn(div_rn(Z.q, rho), rho);
-    }
-    Z.ye = add(add(1.0, mul(1.0e-3, Z.T)), mul(0.1, m));                      // :147-148
-    Z.yp = add(add(add(1.0, mul(8.0e-4, Z.T)), mul(kMC.c005, m)), mul(0.1, sc));  // :156-157
-  }
-  // solve s: 0 = A.entr, 1 = A.prec, 2 = B.entr, 3 = B.prec
-  double t[4], e[4], h[4], y[4], root[4];
-  int cnt[4];
-  unsigned done = 0;
-  bool relax = VAR != kVarApprox && a.relaxed;
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int p = s >> 1;
-    y[s] = (s & 1) ? X[p]->yp : X[p]->ye;
-    t[s] = guess[p];
-    e[s] = e0[p];
-    h[s] = sub(c0[p], y[s]);
-    root[s] = 0.0;
-    cnt[s] = 0;
-    const bool fast = a.fast_div_ok && is_finite(y[s]) && y[s] > -60.0 && y[s] < kBig && h[s] > 0.0 &&
-                      exp_fast_ok(mul(kMC.c005, guess[p]));
-    if (!fast) done |= 1u << s;
-    relax = relax && relaxed_ok(y[s], a.tol);
-  }
-  const unsigned slow = done;
-  if (relax) newton_lockstep<VAR, 4, true>(tab, tab_addr, a.tol, a.maxit, t, e, h, y, root, cnt, done);
-  else newton_lockstep<VAR, 4, false>(tab, tab_addr, a.tol, a.maxit, t, e, h, y, root, cnt, done);
-  A.ok = B.ok = true;
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int p = s >> 1;
-    LevelSolve& Z = *X[p];
-    const long long col = p ? colB : colA;
-    const int order = (s & 1) ? a.L + k : k;
-    if (slow & (1u << s)) {  // restart from the guess: the lockstep steps were not its own
-      t[s] = guess[p];
-      e[s] = e0[p];
-      h[s] = sub(c0[p], y[s]);
-      cnt[s] = 0;
-    }
-    if (!(done & (1u << s)) || (slow & (1u << s))) {
-      // slow-path or unconverged solve: reference-faithful generic loop
-      if (!is_finite(y[s])) {
-        raise_failure(a.err, col, order, kFailInput);
-        Z.ok = false;
-        continue;
-      }
-      if (!newton_generic<VAR>(a, tab, col, order, y[s], t[s], e[s], h[s], cnt[s])) {
-        Z.ok = false;
-        continue;
-      }
-      root[s] = t[s];
-    }
-    if (s & 1) Z.rp = root[s]; else Z.re = root[s];
-  }
-  A.work = cnt[0] + cnt[1];
-  B.work = cnt[2] + cnt[3];
-}
-
-// Pair worker: the warp claims chunks of kDeepChunk list entries (pairs
-// (j, j+1), j even), stages the next pair's (s, T[lane], q[lane]) into its
-// shared double buffer with per-lane cp.async behind the current pair's
-// solves (s_stage: [2][6][32] doubles), and finishes per-column scalars in
-// batches.  L <= 32.
-template <int VAR>
-__device__ __forceinline__ void deep_worker_pairs(const DeepArgs& a, const double2* s_tab, double* s_term,
-                                                  int* s_bcol, int* s_bwork, double* s_stage, int lane) {
-  const int L = a.L;
-  const long long A = *a.count;
-  long long next_raw = 0;
-  const unsigned lane_op = opaque_u32(lane);
-  auto claim = [&]() { if (lane == 0) next_raw = claim_chunk(a.cursor + lane_op); };
-  auto advance = [&](long long x) -> long long {   // next pair start
-    if (((x + 2) & (kDeepChunk - 1)) != 0) return x + 2;
-    const long long r = __shfl_sync(0xffffffffu, next_raw, 0);
-    claim();
-    return r;
-  };
-  unsigned tab_addr;
-  asm volatile("mov.b32 %0, %1;" : "=r"(tab_addr) : "r"((unsigned)__cvta_generic_to_shared(s_tab)));
-  const unsigned st_addr = opaque_u32(smem_u32(s_stage + lane));
-  auto stage = [&](int cA_, int cB_, int b) {   // cB_ < 0: no second column
-    const unsigned d = st_addr + b * 1536;
-    const int cb = cB_ < 0 ? cA_ : cB_;
-    cp_async8_u32(d, a.s + cA_);
-    cp_async8_u32(d + 768, a.s + cb);
-    if (lane < L) {
-      cp_async8_u32(d + 256, a.T + (long long)lane * a.ld_in + cA_);
-      cp_async8_u32(d + 512, a.q + (long long)lane * a.ld_in + cA_);
-      cp_async8_u32(d + 1024, a.T + (long long)lane * a.ld_in + cb);
-      cp_async8_u32(d + 1280, a.q + (long long)lane * a.ld_in + cb);
-    }
-    cp_async_commit();
-  };
-  claim();
-  long long j = __shfl_sync(0xffffffffu, next_raw, 0);
-  claim();
-  long long jn = advance(j);
-  auto col_of = [&](long long x) -> int { return x < A ? a.idx[x] : -1; };
-  int cA = col_of(j), cB = col_of(j + 1), nA = col_of(jn), nB = col_of(jn + 1);
-  int buf = 0;
-  if (cA >= 0) stage(cA, cB, 0);
-  int nb = 0;
-  while (cA >= 0) {
-    // consume the pair staged a pair ago, stage the next one (its indices
-    // were loaded a pair ago), then load the indices of the pair after next
-    cp_async_wait_all();
-    LevelSolve XA, XB;
-    const unsigned d = st_addr + buf * 1536;
-    const double scA = lds_f64(d), scB = lds_f64(d + 768);
-    XA.T = XA.q = XB.T = XB.q = 0.0;
-    if (lane < L) {
-      XA.T = lds_f64(d + 256);
-      XA.q = lds_f64(d + 512);
-      XB.T = lds_f64(d + 1024);
-      XB.q = lds_f64(d + 1280);
-    }
-    if (nA >= 0) stage(nA, nB, buf ^ 1);
-    buf ^= 1;
-    const bool hasB = cB >= 0;
-    const long long jnn = (jn < A) ? advance(jn) : A;
-    const int mA = col_of(jnn), mB = col_of(jnn + 1);
-    XA.work = XB.work = 0;
-    XA.ok = XB.ok = true;
-    double termA = 0.0, termB = 0.0;
-    if (lane < L) {
-      deep_pair_solve<VAR>(a, s_tab, tab_addr, lane, a.first_col + cA, a.first_col + (hasB ? cB : cA), scA,
-                           scB, XA, XB);
-      const int k = lane;
-      // physics.cpp:151-152 / :159-161 for both columns
-      double s1, s2, s3, s4;
-      sin2_cw(add(mul(6.0, XA.T), mul(50.0, XA.q)), mul(3.0, XA.rp), s1, s2);
-      sin2_cw(add(mul(6.0, XB.T), mul(50.0, XB.q)), mul(3.0, XB.rp), s3, s4);
-      if (XA.ok) {
-        const long long o = (long long)k * a.ld_out + cA;
-        a.tend_T[o] = add(mul(0.02, sub(add(250.0, mul(2.0, XA.re)), XA.T)), mul(0.3, s1));
-        a.tend_q[o] = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, s2)), XA.q));
-        termA = mul(XA.q, max0(sub(XA.rp, 4.5)));
-      }
-      if (hasB && XB.ok) {
-        const long long o = (long long)k * a.ld_out + cB;
-        a.tend_T[o] = add(mul(0.02, sub(add(250.0, mul(2.0, XB.re)), XB.T)), mul(0.3, s3));
-        a.tend_q[o] = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, s4)), XB.q));
-        termB = mul(XB.q, max0(sub(XB.rp, 4.5)));
-      }
-      s_term[nb * L + k] = termA;
-      s_term[(nb + 1) * L + k] = termB;
-    }
-    const int wA = __reduce_add_sync(0xffffffffu, XA.work);
-    const int wB = __reduce_add_sync(0xffffffffu, XB.work);
-    const bool okA = __all_sync(0xffffffffu, XA.ok);
-    const bool okB = __all_sync(0xffffffffu, XB.ok);
-    if (lane == 0) {
-      s_bcol[nb] = okA ? cA : -1;
-      s_bwork[nb] = wA;
-      s_bcol[nb + 1] = (hasB && okB) ? cB : -1;
-      s_bwork[nb + 1] = wB;
-    }
-    nb += 2;
-    cA = nA; cB = nB; nA = mA; nB = mB;
-    jn = jnn;
-    if (nb + 2 > a.batch || cA < 0) {
-      __syncwarp();
-      if (lane < nb) {
-        const int cc = s_bcol[lane];
-        if (cc >= 0) {
-          double pr = 0.0;  // ordered k sum, physics.cpp:161
-          const double* tt = s_term + lane * L;
-          for (int kk = 0; kk < L; ++kk) pr = add(pr, tt[kk]);
-          a.precip[cc] = pr;
-          a.work[cc] = s_bwork[lane];
-          a.exited[cc] = 0;
-        }
-      }
-      __syncwarp();
-      nb = 0;
-    }
-  }
+  if (FUSED) while (do_tile()) {}
 }
 
 // ---------------------------------------------------------------------------
@@ -803,11 +601,21 @@ struct SmemRows {
   __device__ __forceinline__ double m(int k) const { return q[k * ld]; }
 };
 
+// The deep zero-fill of a column belongs to the shallow kernel only when its
+// whole column group has no triggered column (the deep kernel writes every
+// column of a triggered group, trigger_groups_kernel).  Callers run with
+// lane == column % 32 inside the warp (group = 4 aligned lanes); lanes of
+// columns >= n are inactive and count as untriggered.
+__device__ __forceinline__ bool group_untriggered(double sc, double thr) {
+  const unsigned b = __ballot_sync(__activemask(), sc > thr);
+  return ((b >> ((threadIdx.x & 31) & ~(kGroupCols - 1))) & ((1u << kGroupCols) - 1)) == 0;
+}
+
 template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO, int STRIDE, class SRC, bool RELAX = false>
 __device__ __forceinline__ void shallow_column_src(const ShallowArgs& a, long long c, double sc,
-                                                   const SRC& src, const double2* tab) {
+                                                   const SRC& src, const double2* tab, bool zero_deep) {
   const int L = a.L;
-  if (DO_DEEP_ZERO && !(sc > a.thr)) {
+  if (DO_DEEP_ZERO && zero_deep) {
 #pragma unroll 10
     for (int k = 0; k < L; ++k) {
       __stcs(&a.d_tend_T[(long long)k * a.d_ld_out + c], 0.0);
@@ -943,8 +751,9 @@ __device__ __forceinline__ void shallow_column_src(const ShallowArgs& a, long lo
 
 template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO, int STRIDE, bool RELAX = false>
 __device__ __forceinline__ void shallow_column(const ShallowArgs& a, long long c, const double2* tab) {
+  const double sc = a.s[c];
   shallow_column_src<VAR, DO_SHALLOW, DO_DEEP_ZERO, STRIDE, GlobalRows, RELAX>(
-      a, c, a.s[c], GlobalRows{a.T + c, a.q + c, a.ld_in}, tab);
+      a, c, sc, GlobalRows{a.T + c, a.q + c, a.ld_in}, tab, group_untriggered(sc, a.thr));
 }
 
 constexpr int kShallowThreads = 128;
@@ -1022,9 +831,10 @@ __global__ void __launch_bounds__(kShTile, 1) shallow_tma_kernel(ShallowArgs a) 
       mbar_wait_parity(&s_bar[stage], (unsigned)((i >> 1) & 1));
       const double* sT = buf + stage * stage_elems + tid;
       shallow_column_src<VAR, true, DO_DEEP_ZERO, 1>(a, c, sc, SmemRows{sT, sT + (size_t)L * kShTile, kShTile},
-                                                     s_tab);
+                                                     s_tab, group_untriggered(sc, a.thr));
     } else {
-      shallow_column_src<VAR, false, DO_DEEP_ZERO, 1>(a, c, sc, GlobalRows{a.T + c, a.q + c, a.ld_in}, s_tab);
+      shallow_column_src<VAR, false, DO_DEEP_ZERO, 1>(a, c, sc, GlobalRows{a.T + c, a.q + c, a.ld_in}, s_tab,
+                                                      group_untriggered(sc, a.thr));
     }
     __syncthreads();  // stage fully consumed before it is refilled
   }
@@ -1038,12 +848,13 @@ __global__ void __launch_bounds__(kShTile, 1) shallow_tma_kernel(ShallowArgs a) 
 // Persistent deep kernel: one block per SM; every warp works the deep list
 // (deep_worker).  kDeepWarps when it runs alone, kDeepWarpsOverlap when the
 // shallow kernel shares the SMs (convgpu.cu, overlap mode).
-// Measured (f02, 1 B200): alone, 16 warps beat 20 and 24 (0.585 vs 0.599 ms
-// at 24 -- fewer, unconstrained warps keep their state in registers); in
-// overlap mode 12 warps (~37K registers) leave room for three 128-thread
-// shallow blocks per SM, enough for the shallow kernel to finish under the
-// deep one (step 0.767 ms, against 0.83 at 16 warps and 0.89 at 20).
-constexpr int kDeepWarps = 16;
+// Measured (f02, 1 B200, grouped sector-wide stores): alone, 20 warps (0.478
+// ms) beat 16 (0.487) and 24 (0.503, register-capped); in overlap mode 12
+// warps (~37K registers) leave room for three 128-thread shallow blocks per
+// SM, enough for the shallow kernel to finish under the deep one (step 0.66
+// ms, against 0.74 at 14 warps and 0.81 at 16, where the shallow blocks
+// starve).
+constexpr int kDeepWarps = 20;
 constexpr int kDeepWarpsOverlap = 12;
 
 // Register cap per thread: the register file divided over one block of NW
@@ -1053,38 +864,50 @@ constexpr int deep_max_regs() {
   return ((65536 / (NW * 32)) & ~7) > 255 ? 255 : ((65536 / (NW * 32)) & ~7);
 }
 
-// Per-warp cp.async staging buffer (doubles): two buffers of (s, T, q) x 32
-// lanes for one column, or x 2 columns for the pair worker; none when wide.
-template <bool NARROW, bool PAIRS>
-__host__ __device__ constexpr int deep_stage_doubles() {
-  return NARROW ? (PAIRS ? 2 * 6 * 32 : 2 * 3 * 32) : 0;
-}
-
-template <int VAR, bool NARROW, int NW, bool PAIRS = false>
-__global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a) {
+// FUSED: also runs the shallow scheme (SH) or only the deep zero-fill (!SH)
+// over 32-column tiles (see deep_worker); b.trace unused.
+template <int VAR, bool NARROW, int NW, bool FUSED = false, bool SH = true, bool RELAX_SH = false>
+__global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a, ShallowArgs b) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (a.trace && threadIdx.x == 0) {
     a.trace[3 * blockIdx.x] = smid();
     a.trace[3 * blockIdx.x + 1] = gtimer();
   }
-  __shared__ int s_bcol[NW][kDeepBatch];
-  __shared__ int s_bwork[NW][kDeepBatch];
-
+  __shared__ int s_gwork[NW][kGroupCols];
+  __shared__ int s_gok[NW][kGroupCols];
+  __shared__ double s_gpr[NW][kGroupCols];
+  // dynamic shared memory: [double-double table x kTabCopies][single-double
+  // table x kTab1Copies][per-warp scratch, deep_warp_doubles each]
   double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
+  double* s_tab1_all = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies);
   if (VAR != kVarApprox) {
     for (int i = threadIdx.x; i < kExpTableSize * kTabCopies; i += blockDim.x)
       s_tab_all[i] = a.exp_tab[i / kTabCopies];
+    for (int i = threadIdx.x; i < kExpTableSize * kTab1Copies; i += blockDim.x)
+      s_tab1_all[i] = a.exp_tab[i / kTab1Copies].x;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const double2* s_tab = s_tab_all + (lane & (kTabCopies - 1));
-  // dynamic shared memory: [table copies][per-warp staging][per-warp batch terms]
-  double* s_stage = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies) +
-                    (size_t)wib * deep_stage_doubles<NARROW, PAIRS>();
-  double* s_term = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies) +
-                   (size_t)NW * deep_stage_doubles<NARROW, PAIRS>() + (size_t)wib * a.batch * a.L;
-  if (PAIRS && NARROW) deep_worker_pairs<VAR>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], s_stage, lane);
-  else deep_worker<VAR, NARROW>(a, s_tab, s_term, s_bcol[wib], s_bwork[wib], s_stage, lane);
+  // opaque, so the lane's address stays in a register rather than being
+  // rematerialised from %tid inside the Newton loop
+  const unsigned tab1_addr = opaque_u32(smem_u32(s_tab1_all + (lane & (kTab1Copies - 1))));
+  double* s_warp = s_tab1_all + kExpTableSize * kTab1Copies + (size_t)wib * deep_warp_doubles(NARROW, a.L);
+  if (FUSED) {
+    const long long ntiles = (b.n + 31) / 32;
+    const long long G = *a.count;
+    const int every = (int)max(1LL, G / max(1LL, ntiles));
+    auto tile = [&](long long tt) -> bool {
+      if (tt >= ntiles) return false;
+      const long long c = tt * 32 + lane;
+      if (c < b.n) shallow_column<VAR, SH, true, 1, RELAX_SH>(b, c, s_tab_all);
+      return true;
+    };
+    deep_worker<VAR, NARROW, true>(a, s_tab, tab1_addr, s_warp, s_gwork[wib], s_gok[wib], s_gpr[wib], lane, tile,
+                                   a.cursor + 16, every);
+  } else {
+    deep_worker<VAR, NARROW>(a, s_tab, tab1_addr, s_warp, s_gwork[wib], s_gok[wib], s_gpr[wib], lane);
+  }
   if (a.trace) {
     __syncthreads();
     if (threadIdx.x == 0) a.trace[3 * blockIdx.x + 2] = gtimer();
