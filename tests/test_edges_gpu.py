@@ -243,3 +243,31 @@ def test_chunked_pipeline_strided_host_rows(small_chunk_ctx):
     got = P.ColumnOutputs(out.tend_T[:, :n], out.tend_q[:, :n], out.precip, out.work_units, out.exited_early)
     both_close(got, od)
     assert not out.tend_T[:, n:].any()
+
+
+def test_nan_activity_in_later_chunk_reports_absolute_column(small_chunk_ctx, ctx):
+    """The trigger kernel keys failures by absolute column id (first_col +
+    offset of the chunk), as the shallow and deep kernels do."""
+    s, T, q = G.make_config("c1", n=4000, seed=8)
+    s[2500] = np.nan
+    for c in (small_chunk_ctx, ctx):
+        with pytest.raises(P.KernelError) as e:
+            c.deep_convection(s, T, q, first_col=7)
+        assert e.value.column == 2507 and "non-finite activity" in str(e.value)
+        with pytest.raises(P.KernelError) as e:
+            c.convect(s, T, q, first_col=7)
+        assert e.value.column == 2507 and "deep" in str(e.value)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 6, 7, 4093])
+def test_group_tails(ctx, n):
+    """Column counts that leave a partial 4-column group at the end; an
+    all-triggered and an all-untriggered grid."""
+    s, T, q = G.make_config("c1", n=max(n, 8), seed=n)
+    s, T, q = s[:n].copy(), np.ascontiguousarray(T[:, :n]), np.ascontiguousarray(q[:, :n])
+    for sv in (None, 0.9, 0.1):
+        if sv is not None:
+            s[:] = sv
+        deep, sh = ctx.convect(s, T, q)
+        both_close(deep, O.convection("deep", s, T, q))
+        both_close(sh, O.convection("shallow", s, T, q))
