@@ -833,6 +833,16 @@ void cvg_host_free(void* p) {
   if (p) cudaFreeHost(p);
 }
 
+#ifdef CVG_PHASE_CLOCKS
+// debug builds: read and reset the deep worker's phase clocks
+cvg_status cvg_debug_phases(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, cvg::g_phase, sizeof(unsigned long long) * 8);
+  const unsigned long long z[8] = {};
+  cudaMemcpyToSymbol(cvg::g_phase, z, sizeof(z));
+  return CVG_OK;
+}
+#endif
+
 cvg_status cvg_plan_partition(long long n, const double* s, double thr, int n_parts, double deep_weight,
                               double shallow_weight, long long* bounds) {
   if (!bounds || (n > 0 && !s && deep_weight > 0.0)) return fail(CVG_ERR_INVALID, "cvg_plan_partition: null argument");

@@ -31,6 +31,17 @@
 namespace cvg {
 
 enum : int { kVarExact = 0, kVarReduced = 1, kVarApprox = 2 };
+
+// Phase-clock instrumentation of the deep worker (debug builds with
+// -DCVG_PHASE_CLOCKS only): per-phase SM cycles summed over warps.
+#ifdef CVG_PHASE_CLOCKS
+__device__ unsigned long long g_phase[8];
+#define CVG_PCLK(v) const long long v = clock64()
+#define CVG_PACC(i, a, b) if (lane == 0) atomicAdd(&g_phase[i], (unsigned long long)((b) - (a)))
+#else
+#define CVG_PCLK(v)
+#define CVG_PACC(i, a, b)
+#endif
 enum : int { kFailNone = 0, kFailActivity = 1, kFailInput = 2, kFailDiverged = 3, kFailNoConv = 4 };
 
 // Failure key: lowest column first, then the solve order the serial
@@ -222,6 +233,7 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
     // noise only; the exact sequence below is the one the reference runs
     const double tol = a.tol;
     const int maxit = a.maxit;
+    CVG_PCLK(pl0);
     int left = maxit + 1;   // updates still allowed (the loop may take one
                             // more than maxit; newton_finish then fails it)
     if (left > 0) do {
@@ -230,6 +242,11 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
       newton_relaxed_step(tp, ep, hp, yp, tab1_addr);
     } while (--left != 0);
     it = maxit + 1 - max(left, 0);
+    {
+      CVG_PCLK(pl1);
+      const int lane = threadIdx.x & 31;
+      CVG_PACC(4, pl0, pl1);   // relaxed Newton loop
+    }
   } else if (fast_ok) {
     const double tol = a.tol;
     const int maxit = a.maxit;
@@ -376,6 +393,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
   long long c = g * kGroupCols + i;
   if (NARROW) stage(c, 0);
   for (;;) {
+    CVG_PCLK(ph0);
     // the column after this one: the group's next, or the next group's first
     long long cn = -1;
     if (rem) cn = g * kGroupCols + (__ffs(rem) - 1);
@@ -399,6 +417,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     const double rho = add(1.0, mul(kMC.c005, sc));
     const double e0 = deep_exp<VAR>(mul(kMC.c005, guess), s_tab);
     const double c0 = add(e0, mul(kMC.c001, guess));
+    CVG_PCLK(ph1);
     const long long col = a.first_col + c;
     int wl = 0;
     bool ok_all = true;
@@ -451,6 +470,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       }
       wl += w;
     }
+    CVG_PCLK(ph3);
     const int wsum = __reduce_add_sync(0xffffffffu, wl);
     const bool ok = __all_sync(0xffffffffu, ok_all);
     if (lane == 0) {
@@ -464,6 +484,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       s_gpr[i] = pr;
     }
     if (!NARROW) __syncwarp();   // s_term is reused by the next column
+    CVG_PCLK(ph4);
     if (rem == 0) {
       // last triggered column of group g: write the group's deep outputs,
       // zeros for its untriggered columns (physics.cpp:89-97)
@@ -525,6 +546,13 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       g = e >> 4;
       m = (unsigned)(e & 15);
       rem = m;
+    }
+    {
+      CVG_PCLK(ph5);
+      CVG_PACC(0, ph0, ph1);   // wait + stage + prologue to col
+      CVG_PACC(1, ph1, ph3);   // per-level: m, ye/yp, Newton, sin, tendencies
+      CVG_PACC(2, ph3, ph4);   // reductions
+      CVG_PACC(3, ph4, ph5);   // group flush + advance
     }
     i = __ffs(rem) - 1;
     rem &= rem - 1;
