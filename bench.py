@@ -411,8 +411,9 @@ def run_gpu_arm(args):
                           "fp64_peak_tflops": fp64_peak,
                           "bound": "fp64" if t_flop >= t_hbm else "hbm",
                           "roofline_ms": 1e3 * t_roof, "frac": 1e3 * t_roof / (ms_total / K) if ws == 1 else None},
-        "kernels_ms": {"trigger_compact": trig_ms, "deep": deep_ms, "shallow_tail_after_deep": sh_ms,
-                       "schedule": "trigger -> deep (main stream) || shallow+zero-fill (side stream, concurrent)"},
+        "kernels_ms": {"trigger_groups": trig_ms, "deep": deep_ms, "shallow_tail_after_deep": sh_ms,
+                       "schedule": "trigger/group compaction -> deep (main stream) || shallow + zero-fill of "
+                                   "untriggered groups (side stream, concurrent)"},
         "gpu_launches": 3 * K,
         "e2e": e2e,
         "cpu_baseline": cpu,

@@ -1,27 +1,29 @@
 // convgpu_kernels.cuh -- sm_100a kernels of the convection column path.
 //
-//   trigger_compact_kernel  deep trigger s > thr (physics.cpp:108-113) with
+//   trigger_groups_kernel   deep trigger s > thr (physics.cpp:108-113) with
 //                           warp-ballot / block-scan stream compaction into a
-//                           dense list of triggered columns (replaces the
-//                           reference's dynamic scheduling, sched.cpp:166-173)
-//   deep_kernel             deep plume (physics.cpp:106-166) over the
-//                           compacted list: one warp per column, one lane per
-//                           level, each lane running its level's entrainment
-//                           and precipitation Newton solves (physics.cpp:
-//                           64-87) in lockstep; persistent warps walk the list
-//                           cyclically with the next column prefetched;
-//                           ordered precip sum per column inside the warp
+//                           dense list of 4-column groups holding a triggered
+//                           column (replaces the reference's dynamic
+//                           scheduling, sched.cpp:166-173)
+//   deep_kernel             deep plume (physics.cpp:106-166) over the group
+//                           list: one warp per column, one lane per level,
+//                           each lane running its level's entrainment and
+//                           precipitation Newton solves (physics.cpp:64-87) in
+//                           lockstep; persistent warps claim groups
+//                           dynamically, stage the next column with cp.async
+//                           and write each group's outputs as whole sectors
 //   shallow_kernel          shallow scheme (physics.cpp:168-225), one thread
 //                           per column, streaming level-major rows, together
-//                           with the zero-fill of untriggered deep columns
-//                           (physics.cpp:89-97, :111-113)
+//                           with the zero-fill of groups without a triggered
+//                           column (physics.cpp:89-97, :111-113)
 //   ientropy_kernel         batched ientropy_solve (physics.cpp:101-104)
 //   approx_exp_kernel       approx_exp (physics.cpp:40-60)
 //
-// Layout: level-major SoA, field[k * ld + c].  Every IEEE operation of the
-// reference is one uncontracted, correctly rounded device operation (see
-// colmath.cuh); outputs therefore match the reference bit for bit except
-// where libm exp/sin enter (Exact/StrengthReduced variants).
+// Layout: level-major SoA, field[k * ld + c].  The strict path performs every
+// IEEE operation of the reference as one uncontracted, correctly rounded
+// device operation (colmath.cuh); the relaxed path (default for the variants
+// whose reference calls libm exp) differs from it only by rounding noise
+// inside the parity window (colmath.cuh, newton_relaxed_step).
 #pragma once
 #include <cstdint>
 
