@@ -43,7 +43,7 @@ typedef enum cvg_status {
   CVG_ERR_INVALID = 1, /* null handle, bad argument, internal failure      */
   CVG_ERR_CONFIG = 2,  /* (reserved; same code as CVP_ERR_CONFIG)          */
   CVG_ERR_NUMERIC = 3, /* kernel numeric failure: NaN, divergence, maxiter  */
-  CVG_ERR_CHECK = 4,   /* (reserved; same code as CVP_ERR_CHECK)           */
+  CVG_ERR_CHECK = 4,   /* validation check failed (divergence, perturbation) */
   CVG_ERR_IO = 5,      /* (reserved; same code as CVP_ERR_IO)              */
   CVG_ERR_DEVICE = 6   /* CUDA runtime failure or no usable sm_100 device  */
 } cvg_status;
@@ -74,7 +74,13 @@ typedef struct cvg_options {
   double activity_threshold; /* default 0.5                       */
   double newton_tol;         /* default 1e-12 (absolute)          */
   int newton_max_iter;       /* default 100                       */
+  int flags;                 /* CVG_FLAG_*, default 0             */
 } cvg_options;
+
+/* cvg_options.flags: reference rounding in every Newton update of every
+ * variant (the default relaxed update of Exact/StrengthReduced differs from
+ * it only by rounding noise inside the parity window). */
+#define CVG_FLAG_STRICT 1
 
 /* Input column block (the SoA form of convproxy::Chunk, physics.hpp:39-43). */
 typedef struct cvg_columns {
@@ -159,6 +165,42 @@ cvg_status cvg_ientropy_solve(cvg_context* ctx, long long n, const double* y,
 /* Device evaluation of approx_exp (physics.hpp:83) over n host values. */
 cvg_status cvg_approx_exp(cvg_context* ctx, long long n, const double* x,
                           double* out);
+
+/* --- Feedback loop (validate.cpp:113-206) ------------------------------ */
+
+/* Device-resident timestep loop: n_steps times, run `kernel` (CVG_DEEP =
+ * deep_column or CVG_SHALLOW = shallow_column) over the state and advance it,
+ * T += tend_T, q += tend_q (validate.cpp:127-136); s is not advanced.  T and
+ * q ([L][ld], host or device per on_device) are updated in place; the state
+ * stays in HBM between steps.  After each step a non-finite T or q returns
+ * CVG_ERR_CHECK ("timestep: state diverged at step <t>", check_finite,
+ * validate.cpp:138-153) with stats->failing_column = -1; a kernel failure
+ * returns CVG_ERR_NUMERIC as cvg_convect does.  stats may be NULL. */
+cvg_status cvg_timestep(cvg_context* ctx, long long n, int n_levels, long long ld, const double* s,
+                        double* T, double* q, int on_device, const cvg_options* opts, int kernel,
+                        int n_steps, cvg_stats* stats);
+
+typedef struct cvg_growth {
+  int envelope_ok;     /* rms_mod[t] <= rms_pert[t] for every t              */
+  double worst_ratio;  /* max over t of rms_mod / rms_pert (validate.cpp:198-204) */
+  int failing_step;    /* timestep of a divergence (CVG_ERR_CHECK), else -1  */
+} cvg_growth;
+
+/* error_growth (validate.hpp:71-82), device-resident: three legs from the
+ * same initial grid for `timesteps` steps of the feedback loop -- baseline
+ * (options `baseline`), modified (options `modified`), perturbed (initial T
+ * with its least significant bit flipped, perturb_lsb, validate.cpp:29-34;
+ * options `baseline`) -- and after every step the RMS difference of the
+ * modified and perturbed legs' temperature fields against the baseline's
+ * (rms_mod[t], rms_pert[t], each of length timesteps).  A non-finite initial
+ * T returns CVG_ERR_CHECK ("perturb_lsb: non-finite value"); a leg whose state
+ * turns non-finite returns CVG_ERR_CHECK ("error_growth: <leg> leg diverged",
+ * out->failing_step = t), checked in the order baseline, modified,
+ * perturbed.  The RMS sums run as a fixed-order tree on the device, so they
+ * differ from the reference's serial sum by rounding only. */
+cvg_status cvg_error_growth(cvg_context* ctx, const cvg_columns* initial, int kernel,
+                            const cvg_options* baseline, const cvg_options* modified, int timesteps,
+                            double* rms_mod, double* rms_pert, cvg_growth* out);
 
 /* Host-side partition of a column block across n_parts devices, balanced by
  * estimated cost w_c = deep_weight * [s_c > thr] + shallow_weight

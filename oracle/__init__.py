@@ -107,6 +107,10 @@ def ref_lib():
                                        C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.POINTER(C.c_double), C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_error_growth.restype = C.c_int
+        L.ref_error_growth.argtypes = [C.c_int, C.c_longlong, C.c_int, _dp, _dp, _dp, C.c_int, C.c_int,
+                                       C.c_double, C.c_double, C.c_int, C.c_int, _dp, _dp,
+                                       C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_int)]
         _ref = L
     return _ref
 
@@ -213,3 +217,33 @@ def ref_time_run_parallel(s, T, q, opts: Options | None = None, n_threads=None,
         return out
     finally:
         R.ref_chunk_free(h)
+
+
+class GrowthSeries:
+    """ErrorGrowthSeries (validate.hpp:64-69) plus the call's status: 0 ok,
+    3 KernelError, 4 ValidationError (fail_step = the failing timestep)."""
+
+    def __init__(self, steps):
+        self.rms_mod = np.zeros(steps)
+        self.rms_pert = np.zeros(steps)
+        self.envelope_ok = True
+        self.worst_ratio = 0.0
+        self.status = 0
+        self.fail_step = -1
+
+
+def ref_error_growth(kernel: str, s, T, q, base_variant=EXACT, mod_variant=EXACT, timesteps=50,
+                     opts: Options | None = None) -> GrowthSeries:
+    """The reference's own error_growth (validate.cpp:168-206) on a SoA grid:
+    baseline / modified variants, serial StaticBlock paths."""
+    opts = opts or Options()
+    s, T, q = _soa(s, T, q)
+    L, n = T.shape
+    g = GrowthSeries(timesteps)
+    env, worst, fs = C.c_int(), C.c_double(), C.c_int(-1)
+    g.status = ref_lib().ref_error_growth(0 if kernel == "deep" else 1, n, L, s, T, q, base_variant,
+                                          mod_variant, opts.activity_threshold, opts.newton_tol,
+                                          opts.newton_max_iter, timesteps, g.rms_mod, g.rms_pert,
+                                          C.byref(env), C.byref(worst), C.byref(fs))
+    g.envelope_ok, g.worst_ratio, g.fail_step = bool(env.value), worst.value, fs.value
+    return g

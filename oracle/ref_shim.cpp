@@ -1,7 +1,7 @@
 // ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
 //
 // A C-ABI shim, written for this repo, over the UNMODIFIED reference sources
-// /root/reference/proj/src/core/{physics,sched}.cpp, which oracle/Makefile
+// /root/reference/proj/src/core/{physics,sched,validate,hetero}.cpp, which oracle/Makefile
 // compiles in place (read-only) into oracle/_ref/libconvref.so with the
 // reference's own flags (-std=c++20 -O3 -DNDEBUG -ffp-contract=off,
 // proj/CMakeLists.txt:12-15).  No reference source is copied into this repo.
@@ -21,6 +21,7 @@
 #include "errors.hpp"
 #include "physics.hpp"
 #include "sched.hpp"
+#include "validate.hpp"
 
 using namespace convproxy;
 
@@ -173,6 +174,43 @@ int ref_run_parallel(void* h, int kernel, int variant, double thr, double tol,
     return 0;
   } catch (const KernelError&) {
     return 3;
+  } catch (...) {
+    return 1;
+  }
+}
+
+// ---- error_growth (validate.cpp:168-206) -----------------------------------
+//
+// Three legs from the same grid for `timesteps` steps of T += tend_T,
+// q += tend_q with kernel deep_column (0) or shallow_column (1): baseline
+// (variant vb), modified (variant vm), perturbed (initial T one ulp off,
+// variant vb).  Both paths serial StaticBlock, as acceptance.cpp:570-573.
+// Returns 0 ok, 3 KernelError, 4 ValidationError (*fail_step set), 1 other.
+int ref_error_growth(int kernel, long long n, int L, const double* s, const double* T, const double* q,
+                     int vb, int vm, double thr, double tol, int maxit, int timesteps, double* rms_mod,
+                     double* rms_pert, int* envelope_ok, double* worst_ratio, int* fail_step) {
+  try {
+    const Chunk ch = to_chunk(n, L, n, 0, s, T, q);
+    SimPath base;
+    base.opts = make_opts(vb, thr, tol, maxit);
+    base.sched.strategy = Strategy::StaticBlock;
+    base.sched.n_threads = 1;
+    SimPath mod = base;
+    mod.opts = make_opts(vm, thr, tol, maxit);
+    const KernelFn fn = kernel == 0 ? &deep_column : &shallow_column;
+    const ErrorGrowthSeries r = error_growth(ch, fn, base, mod, timesteps);
+    for (size_t i = 0; i < r.rms_mod.size(); ++i) {
+      rms_mod[i] = r.rms_mod[i];
+      rms_pert[i] = r.rms_pert[i];
+    }
+    *envelope_ok = r.envelope_ok ? 1 : 0;
+    *worst_ratio = r.worst_ratio;
+    return 0;
+  } catch (const KernelError&) {
+    return 3;
+  } catch (const ValidationError& e) {
+    if (fail_step) *fail_step = e.timestep();
+    return 4;
   } catch (...) {
     return 1;
   }

@@ -23,7 +23,8 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = [
-    "Variant", "KernelOptions", "KernelError", "DeviceError", "ColumnOutputs", "Stats",
+    "Variant", "KernelOptions", "KernelError", "DeviceError", "ValidationError", "ColumnOutputs", "Stats",
+    "GrowthSeries",
     "Context", "deep_convection", "shallow_convection", "ientropy_solve", "approx_exp",
     "plan_partition", "library_path", "load_library", "DEEP", "SHALLOW", "BOTH",
 ]
@@ -40,19 +41,23 @@ class Variant:
     APPROX_TRANSCENDENTAL = 2
 
 
+FLAG_STRICT = 1
+
+
 class KernelOptions(C.Structure):
-    """convproxy::KernelOptions (physics.hpp:68-73), same defaults."""
+    """convproxy::KernelOptions (physics.hpp:68-73), same defaults, plus
+    ``strict``: reference rounding in every Newton update (CVG_FLAG_STRICT)."""
     _fields_ = [("variant", C.c_int), ("activity_threshold", C.c_double),
-                ("newton_tol", C.c_double), ("newton_max_iter", C.c_int)]
+                ("newton_tol", C.c_double), ("newton_max_iter", C.c_int), ("flags", C.c_int)]
 
     def __init__(self, variant=Variant.EXACT, activity_threshold=0.5, newton_tol=1e-12,
-                 newton_max_iter=100):
+                 newton_max_iter=100, strict=False):
         super().__init__(int(variant), float(activity_threshold), float(newton_tol),
-                         int(newton_max_iter))
+                         int(newton_max_iter), FLAG_STRICT if strict else 0)
 
     def __repr__(self):
         return (f"KernelOptions(variant={self.variant}, activity_threshold={self.activity_threshold},"
-                f" newton_tol={self.newton_tol}, newton_max_iter={self.newton_max_iter})")
+                f" newton_tol={self.newton_tol}, newton_max_iter={self.newton_max_iter}, flags={self.flags})")
 
 
 class _Columns(C.Structure):
@@ -74,7 +79,7 @@ class Stats(C.Structure):
                 ("d2h_ms", C.c_double), ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong)]
 
 
-CVG_OK, CVG_ERR_INVALID, CVG_ERR_NUMERIC, CVG_ERR_DEVICE = 0, 1, 3, 6
+CVG_OK, CVG_ERR_INVALID, CVG_ERR_NUMERIC, CVG_ERR_CHECK, CVG_ERR_DEVICE = 0, 1, 3, 4, 6
 
 
 class KernelError(RuntimeError):
@@ -89,6 +94,30 @@ class KernelError(RuntimeError):
 
 class DeviceError(RuntimeError):
     pass
+
+
+class ValidationError(RuntimeError):
+    """A validation check failed (CVG_ERR_CHECK; the reference's
+    ValidationError, errors.hpp:58-70): a diverged feedback-loop state or a
+    non-finite value handed to perturb_lsb.  ``timestep`` is the failing step
+    (-1 when not applicable)."""
+
+    def __init__(self, msg, timestep=-1):
+        super().__init__(msg)
+        self.timestep = timestep
+
+
+class _Growth(C.Structure):
+    _fields_ = [("envelope_ok", C.c_int), ("worst_ratio", C.c_double), ("failing_step", C.c_int)]
+
+
+@dataclass
+class GrowthSeries:
+    """convproxy::ErrorGrowthSeries (validate.hpp:64-69)."""
+    rms_mod: np.ndarray
+    rms_pert: np.ndarray
+    envelope_ok: bool
+    worst_ratio: float
 
 
 def library_path() -> str:
@@ -131,10 +160,14 @@ def load_library():
     L.cvg_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
     L.cvg_host_free.argtypes = [vp]
     L.cvg_host_free.restype = None
+    L.cvg_timestep.argtypes = [vp, i64, i32, i64, vp, vp, vp, i32, C.POINTER(KernelOptions), i32, i32,
+                               C.POINTER(Stats)]
+    L.cvg_error_growth.argtypes = [vp, C.POINTER(_Columns), i32, C.POINTER(KernelOptions),
+                                   C.POINTER(KernelOptions), i32, vp, vp, C.POINTER(_Growth)]
     for f in ("cvg_profile_begin", "cvg_profile_end", "cvg_fp64_peak", "cvg_host_alloc",
               "cvg_context_create", "cvg_convect", "cvg_convect_async", "cvg_convect_check",
               "cvg_deep_convection", "cvg_shallow_convection", "cvg_ientropy_solve",
-              "cvg_approx_exp", "cvg_plan_partition"):
+              "cvg_approx_exp", "cvg_plan_partition", "cvg_timestep", "cvg_error_growth"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -150,6 +183,8 @@ def _raise(rc, stats: Stats | None = None):
         raise KernelError(msg, col, kind)
     if rc == CVG_ERR_DEVICE:
         raise DeviceError(msg)
+    if rc == CVG_ERR_CHECK:
+        raise ValidationError(msg)
     raise ValueError(f"convgpu status {rc}: {msg}")
 
 
@@ -253,6 +288,41 @@ class Context:
         out = np.empty_like(x)
         _raise(load_library().cvg_approx_exp(self._h, x.size, x.ctypes.data, out.ctypes.data))
         return out
+
+    # -- feedback loop (validate.cpp:113-206) ---------------------------------
+    def timestep(self, s, T, q, opts: KernelOptions | None = None, kernel=DEEP, n_steps=1):
+        """n_steps of the device-resident loop T += tend_T, q += tend_q with
+        the deep (DEEP) or shallow (SHALLOW) kernel; returns the new (T, q)
+        (host copies; the inputs are not modified)."""
+        opts = opts or KernelOptions()
+        s = np.ascontiguousarray(s, dtype=np.float64)
+        T = np.array(T, dtype=np.float64, order="C", copy=True)
+        q = np.array(q, dtype=np.float64, order="C", copy=True)
+        L, n = T.shape
+        st = Stats()
+        rc = load_library().cvg_timestep(self._h, n, L, n, s.ctypes.data, T.ctypes.data, q.ctypes.data, 0,
+                                         C.byref(opts), int(kernel), int(n_steps), C.byref(st))
+        self.last_stats = st
+        _raise(rc, st)
+        return T, q
+
+    def error_growth(self, s, T, q, kernel=DEEP, baseline: KernelOptions | None = None,
+                     modified: KernelOptions | None = None, timesteps=50) -> GrowthSeries:
+        """error_growth (validate.hpp:71-82) on the device: baseline, modified
+        and LSB-perturbed legs; raises ValidationError (with .timestep) when a
+        leg diverges."""
+        baseline = baseline or KernelOptions()
+        modified = modified or KernelOptions()
+        keep, cols = _host_columns(s, T, q, 0)
+        rm, rp = np.zeros(max(timesteps, 0)), np.zeros(max(timesteps, 0))
+        g = _Growth()
+        rc = load_library().cvg_error_growth(self._h, C.byref(cols), int(kernel), C.byref(baseline),
+                                             C.byref(modified), int(timesteps), rm.ctypes.data, rp.ctypes.data,
+                                             C.byref(g))
+        if rc == CVG_ERR_CHECK:
+            raise ValidationError(load_library().cvg_last_error().decode(), g.failing_step)
+        _raise(rc)
+        return GrowthSeries(rm, rp, bool(g.envelope_ok), g.worst_ratio)
 
     # -- device-resident entry points (torch CUDA tensors or raw pointers) ----
     def convect_async(self, s, T, q, deep, shallow, opts: KernelOptions | None = None,

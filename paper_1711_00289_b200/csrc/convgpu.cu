@@ -199,6 +199,7 @@ bool valid_outputs(const cvg_outputs* o, long long n, std::string* why) {
 
 bool valid_options(const cvg_options* o, std::string* why) {
   if (o->variant < 0 || o->variant > 2) { *why = "unknown variant"; return false; }
+  if (o->flags & ~CVG_FLAG_STRICT) { *why = "unknown flags"; return false; }
   return true;
 }
 
@@ -223,10 +224,10 @@ void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st,
 // HBM-bound kernel share the SMs), else after it on `st`.
 template <int VAR>
 void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh,
-                    bool dp, cudaEvent_t* pe, cudaStream_t st) {
+                    bool dp, cudaEvent_t* pe, cudaStream_t st, bool strict) {
   if (ctx->fused && dp && a.L <= 32) {
     // one kernel: deep groups with shallow tiles interleaved
-    const bool relax = VAR != cvg::kVarApprox && !ctx->strict;
+    const bool relax = VAR != cvg::kVarApprox && !strict;
     if (sh && relax) launch_deep_t<VAR, true, 20, true, true, true>(ctx, a, st, b);
     else if (sh) launch_deep_t<VAR, true, 20, true, true, false>(ctx, a, st, b);
     else launch_deep_t<VAR, true, 20, true, false, false>(ctx, a, st, b);
@@ -268,7 +269,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     k<<<ctx->num_sms, cvg::kShTile, smem, st>>>(b);
   } else {
     const unsigned blocks = (unsigned)((b.n + cvg::kShallowThreads - 1) / cvg::kShallowThreads);
-    const bool relax = VAR != cvg::kVarApprox && !ctx->strict;
+    const bool relax = VAR != cvg::kVarApprox && !strict;
     if (sh && relax) {
       if (dp && ctx->shallow_minb == 12) cvg::shallow_kernel<VAR, true, true, true, 12><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
       else if (dp && ctx->shallow_minb == 16) cvg::shallow_kernel<VAR, true, true, true, 16><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
@@ -303,6 +304,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
   CVG_CUDA(cudaMemsetAsync(w.err.p, 0xff, 2 * sizeof(unsigned long long), st));
   if (n == 0) return;
   const bool do_deep = (mask & CVG_DEEP) != 0, do_sh = (mask & CVG_SHALLOW) != 0;
+  const bool strict = ctx->strict || (o->flags & CVG_FLAG_STRICT) != 0;
   if (pe) CVG_CUDA(cudaEventRecord(pe[0], st));
   cvg::DeepArgs a{};
   if (do_deep) {
@@ -320,7 +322,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.thr = o->activity_threshold; a.tol = o->newton_tol; a.maxit = o->newton_max_iter;
     a.L = L;
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
-    a.relaxed = !ctx->strict;
+    a.relaxed = !strict;
   }
   a.exp_tab = ctx->exp_tab.p;
   if (pe) CVG_CUDA(cudaEventRecord(pe[1], st));
@@ -345,9 +347,9 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     b.trace = ctx->trace_s.p;
   }
   switch (o->variant) {
-    case 1: launch_kernels<cvg::kVarReduced>(ctx, w, a, b, do_sh, do_deep, pe, st); break;
-    case 2: launch_kernels<cvg::kVarApprox>(ctx, w, a, b, do_sh, do_deep, pe, st); break;
-    default: launch_kernels<cvg::kVarExact>(ctx, w, a, b, do_sh, do_deep, pe, st); break;
+    case 1: launch_kernels<cvg::kVarReduced>(ctx, w, a, b, do_sh, do_deep, pe, st, strict); break;
+    case 2: launch_kernels<cvg::kVarApprox>(ctx, w, a, b, do_sh, do_deep, pe, st, strict); break;
+    default: launch_kernels<cvg::kVarExact>(ctx, w, a, b, do_sh, do_deep, pe, st, strict); break;
   }
 }
 
@@ -436,6 +438,7 @@ void cvg_default_options(cvg_options* o) {
   o->activity_threshold = 0.5;
   o->newton_tol = 1e-12;
   o->newton_max_iter = 100;
+  o->flags = 0;
 }
 
 cvg_status cvg_context_create(int device, cvg_context** out) {
@@ -831,6 +834,231 @@ cvg_status cvg_host_alloc(size_t bytes, void** out) {
 
 void cvg_host_free(void* p) {
   if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"
+
+// --- feedback loop ----------------------------------------------------------
+
+namespace {
+
+// Device state of one leg: T, q [L][n] (ld = n) and the selected kernel's
+// outputs.
+struct LegBufs {
+  DevBuf<double> T, q;
+};
+
+struct LoopBufs {
+  DevBuf<double> s, oT, oq, op;
+  DevBuf<long long> ow;
+  DevBuf<uint8_t> ox;
+  cvg_outputs outs(long long n) {
+    return cvg_outputs{oT.p, oq.p, op.p, ow.p, ox.p, n, 1};
+  }
+  void ensure(long long n, int L) {
+    s.ensure(n); oT.ensure((size_t)n * L); oq.ensure((size_t)n * L); op.ensure(n); ow.ensure(n); ox.ensure(n);
+  }
+};
+
+unsigned elem_blocks(long long n, int L) { return (unsigned)((n * L + 255) / 256); }
+
+// One step of `kernel` over a device leg, its failure words copied to
+// err_slot, then advance with the non-finite flag in *flag.
+void leg_step(cvg_context* ctx, const cvg_options* o, int kernel, long long n, int L, const double* s,
+              LegBufs& leg, LoopBufs& lb, unsigned long long* err_slot, unsigned* flag, cudaStream_t st) {
+  Workspace& w = ctx->ws[0];
+  const cvg_columns in{n, L, 0, n, s, leg.T.p, leg.q.p, 1};
+  const cvg_outputs out = lb.outs(n);
+  enqueue(ctx, w, &in, o, kernel, kernel == CVG_DEEP ? &out : nullptr, kernel == CVG_SHALLOW ? &out : nullptr, st,
+          nullptr);
+  CVG_CUDA(cudaMemcpyAsync(err_slot, w.err.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+  if (n > 0) {
+    cvg::advance_kernel<<<elem_blocks(n, L), 256, 0, st>>>(leg.T.p, leg.q.p, n, lb.oT.p, lb.oq.p, n, n, L, flag);
+    CVG_CUDA(cudaGetLastError());
+  }
+}
+
+// Reads the legs' failure words (in leg order) and raises the first kernel
+// failure as cvg_convect would.
+cvg_status leg_errors(const unsigned long long* h_err, int nlegs, int kernel, int maxit, long long n) {
+  for (int l = 0; l < nlegs; ++l) {
+    const unsigned long long* e = h_err + 2 * l;
+    if (e[0] != ~0ULL || e[1] != ~0ULL) return collect(&e[0], &e[1], 0, kernel, maxit, n, nullptr);
+  }
+  return CVG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+cvg_status cvg_timestep(cvg_context* ctx, long long n, int L, long long ld, const double* s, double* T,
+                        double* q, int on_device, const cvg_options* opts, int kernel, int n_steps,
+                        cvg_stats* stats) {
+  if (!ctx || !opts || (n > 0 && (!s || !T || !q))) return fail(CVG_ERR_INVALID, "cvg_timestep: null argument");
+  std::string why;
+  const cvg_columns probe{n, L, 0, ld, s, T, q, on_device};
+  if (!valid_columns(&probe, &why) || !valid_options(opts, &why)) return fail(CVG_ERR_INVALID, "cvg_timestep: " + why);
+  if (kernel != CVG_DEEP && kernel != CVG_SHALLOW)
+    return fail(CVG_ERR_INVALID, "cvg_timestep: kernel must be CVG_DEEP or CVG_SHALLOW");
+  if (n_steps < 0) return fail(CVG_ERR_INVALID, "cvg_timestep: n_steps < 0");
+  return guarded([&] {
+    CVG_CUDA(cudaSetDevice(ctx->device));
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (stats) stats->failing_column = -1;
+    cudaStream_t st = ctx->stream;
+    LoopBufs lb;
+    LegBufs leg;
+    DevBuf<unsigned long long> err;
+    DevBuf<unsigned> flag;
+    struct Free {
+      LoopBufs& lb; LegBufs& leg; DevBuf<unsigned long long>& err; DevBuf<unsigned>& flag;
+      ~Free() {
+        for (auto* b : {&lb.s, &lb.oT, &lb.oq, &lb.op, &leg.T, &leg.q}) b->release();
+        lb.ow.release(); lb.ox.release(); err.release(); flag.release();
+      }
+    } guard{lb, leg, err, flag};
+    lb.ensure(std::max(n, 1LL), L);
+    leg.T.ensure((size_t)std::max(n, 1LL) * L);
+    leg.q.ensure((size_t)std::max(n, 1LL) * L);
+    err.ensure(2);
+    flag.ensure(1);
+    const cudaMemcpyKind kin = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const cudaMemcpyKind kout = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (n > 0) {
+      CVG_CUDA(cudaMemcpyAsync(lb.s.p, s, sizeof(double) * n, kin, st));
+      CVG_CUDA(cudaMemcpy2DAsync(leg.T.p, sizeof(double) * n, T, sizeof(double) * ld, sizeof(double) * n, L, kin, st));
+      CVG_CUDA(cudaMemcpy2DAsync(leg.q.p, sizeof(double) * n, q, sizeof(double) * ld, sizeof(double) * n, L, kin, st));
+    }
+    CVG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(unsigned), st));
+    cvg_status rc = CVG_OK;
+    for (int t = 0; t < n_steps && n > 0; ++t) {
+      leg_step(ctx, opts, kernel, n, L, lb.s.p, leg, lb, err.p, flag.p, st);
+      unsigned long long h_err[2];
+      unsigned h_flag = 0;
+      CVG_CUDA(cudaMemcpyAsync(h_err, err.p, sizeof(h_err), cudaMemcpyDeviceToHost, st));
+      CVG_CUDA(cudaMemcpyAsync(&h_flag, flag.p, sizeof(h_flag), cudaMemcpyDeviceToHost, st));
+      CVG_CUDA(cudaStreamSynchronize(st));
+      rc = leg_errors(h_err, 1, kernel, opts->newton_max_iter, n);
+      if (rc != CVG_OK) {
+        if (stats) stats->failing_column = (long long)(std::min(h_err[0], h_err[1]) >> 16);
+        return rc;
+      }
+      if (h_flag) return fail(CVG_ERR_CHECK, "timestep: state diverged at step " + std::to_string(t));
+    }
+    if (n > 0) {
+      CVG_CUDA(cudaMemcpy2DAsync(T, sizeof(double) * ld, leg.T.p, sizeof(double) * n, sizeof(double) * n, L, kout, st));
+      CVG_CUDA(cudaMemcpy2DAsync(q, sizeof(double) * ld, leg.q.p, sizeof(double) * n, sizeof(double) * n, L, kout, st));
+    }
+    CVG_CUDA(cudaStreamSynchronize(st));
+    if (stats) stats->n_columns = n;
+    return CVG_OK;
+  });
+}
+
+cvg_status cvg_error_growth(cvg_context* ctx, const cvg_columns* init, int kernel, const cvg_options* base,
+                            const cvg_options* mod, int timesteps, double* rms_mod, double* rms_pert,
+                            cvg_growth* out) {
+  if (!ctx || !init || !base || !mod || !out || (timesteps > 0 && (!rms_mod || !rms_pert)))
+    return fail(CVG_ERR_INVALID, "cvg_error_growth: null argument");
+  std::string why;
+  if (!valid_columns(init, &why) || !valid_options(base, &why) || !valid_options(mod, &why))
+    return fail(CVG_ERR_INVALID, "cvg_error_growth: " + why);
+  if (kernel != CVG_DEEP && kernel != CVG_SHALLOW)
+    return fail(CVG_ERR_INVALID, "cvg_error_growth: kernel must be CVG_DEEP or CVG_SHALLOW");
+  if (timesteps < 0) return fail(CVG_ERR_INVALID, "cvg_error_growth: timesteps < 0");
+  out->envelope_ok = 1;
+  out->worst_ratio = 0.0;
+  out->failing_step = -1;
+  return guarded([&] {
+    CVG_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const long long n = init->n_columns;
+    const int L = init->n_levels;
+    const long long nn = std::max(n, 1LL);
+    LoopBufs lb;
+    LegBufs legs[3];   // baseline, modified, perturbed
+    DevBuf<unsigned long long> err;
+    DevBuf<unsigned> flags;
+    DevBuf<double> partials, sums;
+    struct Free {
+      LoopBufs& lb; LegBufs* legs; DevBuf<unsigned long long>& err; DevBuf<unsigned>& flags;
+      DevBuf<double>& partials; DevBuf<double>& sums;
+      ~Free() {
+        for (auto* b : {&lb.s, &lb.oT, &lb.oq, &lb.op, &partials, &sums}) b->release();
+        lb.ow.release(); lb.ox.release(); err.release(); flags.release();
+        for (int l = 0; l < 3; ++l) { legs[l].T.release(); legs[l].q.release(); }
+      }
+    } guard{lb, legs, err, flags, partials, sums};
+    lb.ensure(nn, L);
+    for (auto& leg : legs) { leg.T.ensure((size_t)nn * L); leg.q.ensure((size_t)nn * L); }
+    err.ensure(6);
+    flags.ensure(4);
+    const int rb = (int)std::min<long long>(4 * ctx->num_sms, std::max(1LL, (n * L + cvg::kRmsThreads - 1) / cvg::kRmsThreads));
+    partials.ensure(2 * (size_t)rb);
+    sums.ensure(2 * (size_t)std::max(timesteps, 1));
+    const cudaMemcpyKind kin = init->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (n > 0) {
+      CVG_CUDA(cudaMemcpyAsync(lb.s.p, init->s, sizeof(double) * n, kin, st));
+      for (auto& leg : legs) {
+        CVG_CUDA(cudaMemcpy2DAsync(leg.T.p, sizeof(double) * n, init->T, sizeof(double) * init->ld, sizeof(double) * n,
+                                   L, kin, st));
+        CVG_CUDA(cudaMemcpy2DAsync(leg.q.p, sizeof(double) * n, init->q, sizeof(double) * init->ld, sizeof(double) * n,
+                                   L, kin, st));
+      }
+    }
+    CVG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(unsigned), st));
+    if (n > 0) {   // perturbed leg: T one ulp off everywhere (validate.cpp:174-177)
+      cvg::perturb_lsb_kernel<<<elem_blocks(n, L), 256, 0, st>>>(legs[2].T.p, n, n, L, flags.p + 3);
+      CVG_CUDA(cudaGetLastError());
+    }
+    unsigned h_flags[4] = {};
+    CVG_CUDA(cudaMemcpyAsync(h_flags, flags.p, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+    CVG_CUDA(cudaStreamSynchronize(st));
+    if (h_flags[3]) return fail(CVG_ERR_CHECK, "perturb_lsb: non-finite value");
+    const cvg_options* leg_opts[3] = {base, mod, base};
+    const char* leg_name[3] = {"baseline", "modified", "perturbed"};
+    for (int t = 0; t < timesteps; ++t) {
+      if (n > 0) {
+        for (int l = 0; l < 3; ++l)
+          leg_step(ctx, leg_opts[l], kernel, n, L, lb.s.p, legs[l], lb, err.p + 2 * l, flags.p + l, st);
+        cvg::rms_partial_kernel<<<rb, cvg::kRmsThreads, 0, st>>>(legs[0].T.p, legs[1].T.p, legs[2].T.p, n, n, L,
+                                                                 partials.p);
+        cvg::rms_final_kernel<<<1, 32, 0, st>>>(partials.p, rb, sums.p + 2 * t);
+        CVG_CUDA(cudaGetLastError());
+      }
+      unsigned long long h_err[6];
+      CVG_CUDA(cudaMemcpyAsync(h_err, err.p, sizeof(h_err), cudaMemcpyDeviceToHost, st));
+      CVG_CUDA(cudaMemcpyAsync(h_flags, flags.p, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      CVG_CUDA(cudaStreamSynchronize(st));
+      if (n > 0) {
+        for (int l = 0; l < 3; ++l) {   // run_path of each leg in order (validate.cpp:183-185)
+          cvg_status rc = leg_errors(h_err + 2 * l, 1, kernel, leg_opts[l]->newton_max_iter, n);
+          if (rc != CVG_OK) return rc;
+        }
+      }
+      for (int l = 0; l < 3; ++l) {    // check_finite in order (:186-188)
+        if (h_flags[l]) {
+          out->failing_step = t;
+          return fail(CVG_ERR_CHECK, std::string("error_growth: ") + leg_name[l] + " leg diverged");
+        }
+      }
+    }
+    std::vector<double> h_sums(2 * (size_t)std::max(timesteps, 1), 0.0);
+    if (timesteps > 0 && n > 0)
+      CVG_CUDA(cudaMemcpy(h_sums.data(), sums.p, sizeof(double) * 2 * timesteps, cudaMemcpyDeviceToHost));
+    const double cnt = (double)(n * L);
+    for (int t = 0; t < timesteps; ++t) {   // validate.cpp:190-205
+      const double rm = n > 0 ? std::sqrt(h_sums[2 * t] / cnt) : 0.0;
+      const double rp = n > 0 ? std::sqrt(h_sums[2 * t + 1] / cnt) : 0.0;
+      rms_mod[t] = rm;
+      rms_pert[t] = rp;
+      if (rm > rp) out->envelope_ok = 0;
+      const double ratio = rp > 0.0 ? rm / rp : (rm > 0.0 ? std::numeric_limits<double>::infinity() : 0.0);
+      if (ratio > out->worst_ratio) out->worst_ratio = ratio;
+    }
+    return CVG_OK;
+  });
 }
 
 #ifdef CVG_PHASE_CLOCKS

@@ -945,6 +945,83 @@ __global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a, Shallow
 }
 
 // ---------------------------------------------------------------------------
+// Feedback loop (validate.cpp:113-206): perturb_lsb, advance, check_finite
+// and the RMS difference of two temperature fields.
+
+// T[k][c] -> bits ^ 1 (perturb_lsb, validate.cpp:29-34); a non-finite value
+// sets *bad (the reference throws ValidationError).
+__global__ void perturb_lsb_kernel(double* T, long long ld, long long n, int L, unsigned* bad) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * L) return;
+  const long long k = i / n, c = i - k * n;
+  double* p = T + k * ld + c;
+  const double x = *p;
+  if (!is_finite(x)) atomicOr(bad, 1u);
+  *p = __longlong_as_double(__double_as_longlong(x) ^ 1LL);
+}
+
+// T += tend_T, q += tend_q (advance, validate.cpp:127-136), one rounding
+// each; a non-finite result sets *nonfinite (check_finite, :138-153).
+__global__ void advance_kernel(double* T, double* q, long long ld, const double* __restrict__ tT,
+                               const double* __restrict__ tq, long long ld_t, long long n, int L,
+                               unsigned* nonfinite) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * L) return;
+  const long long k = i / n, c = i - k * n;
+  const double a = add(T[k * ld + c], tT[k * ld_t + c]);
+  const double b = add(q[k * ld + c], tq[k * ld_t + c]);
+  T[k * ld + c] = a;
+  q[k * ld + c] = b;
+  if (!is_finite(a) || !is_finite(b)) atomicOr(nonfinite, 1u);
+}
+
+// Sums of (Tm - Tb)^2 and (Tp - Tb)^2 over the [L][n] fields, in a fixed
+// order (deterministic): block b reduces elements b, b + G, ... in a tree;
+// rms_final_kernel adds the G partials in block order.
+constexpr int kRmsThreads = 256;
+
+__global__ void __launch_bounds__(kRmsThreads) rms_partial_kernel(const double* Tb, const double* Tm, const double* Tp,
+                                                                  long long ld, long long n, int L,
+                                                                  double* partials) {
+  __shared__ double s0[kRmsThreads], s1[kRmsThreads];
+  double a0 = 0.0, a1 = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n * L;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long k = i / n, c = i - k * n;
+    const double b = Tb[k * ld + c];
+    const double dm = sub(Tm[k * ld + c], b), dp = sub(Tp[k * ld + c], b);
+    a0 = add(a0, mul(dm, dm));
+    a1 = add(a1, mul(dp, dp));
+  }
+  s0[threadIdx.x] = a0;
+  s1[threadIdx.x] = a1;
+  __syncthreads();
+  for (int o = kRmsThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s0[threadIdx.x] = add(s0[threadIdx.x], s0[threadIdx.x + o]);
+      s1[threadIdx.x] = add(s1[threadIdx.x], s1[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = s0[0];
+    partials[2 * blockIdx.x + 1] = s1[0];
+  }
+}
+
+__global__ void rms_final_kernel(const double* partials, int nblocks, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double a0 = 0.0, a1 = 0.0;
+    for (int b = 0; b < nblocks; ++b) {
+      a0 = add(a0, partials[2 * b]);
+      a1 = add(a1, partials[2 * b + 1]);
+    }
+    out[0] = a0;
+    out[1] = a1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Batched inverse-entropy solve (physics.cpp:101-104), one thread per pair.
 template <int VAR>
 __global__ void ientropy_kernel(const double* __restrict__ y, const double* __restrict__ g,

@@ -229,3 +229,15 @@ def test_newton_margin_classifier_is_recorded():
     act = r.exited == 0
     assert np.isfinite(r.margin[act]).all() and (r.margin[act] >= 0).all()
     assert np.isinf(r.margin[~act]).all()
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference build missing")
+def test_reference_error_growth_c11():
+    """acceptance.cpp:595-613 on the reference build: both answer-changing
+    variants stay inside the perturbation envelope, which does not vanish."""
+    s, T, q = O.make_grid(64, 30, 0.3, 42)
+    for v in (O.STRENGTH_REDUCED, O.APPROX_TRANSCENDENTAL):
+        g = O.ref_error_growth("deep", s, T, q, O.EXACT, v, 50)
+        assert g.status == 0 and g.envelope_ok and g.rms_pert[-1] > 0.0
+    g = O.ref_error_growth("deep", s, T, q, O.EXACT, O.EXACT, 10)
+    assert (g.rms_mod == 0.0).all()
