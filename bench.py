@@ -384,6 +384,23 @@ def run_gpu_arm(args):
         for a in pin + pdo + pso:
             a.free()
 
+    # ---- device-resident feedback loop (cvg_timestep): the
+    # per-step cost is the difference of a 42-step and a 2-step call (the
+    # state's H2D / D2H and the buffer set-up happen once per call and cancel)
+    loop = None
+    if not args.no_loop and ws == 1:
+        def loop_s(k):
+            t0 = time.perf_counter()
+            ctx.timestep(s_r, T_r, q_r, opts, P.DEEP, k)
+            return time.perf_counter() - t0
+        loop_s(1)
+        a2, a42 = min(loop_s(2) for _ in range(3)), min(loop_s(42) for _ in range(3))
+        per = max(a42 - a2, 1e-9) / 40
+        loop = {"kernel": "deep", "ms_per_step": 1e3 * per, "columns_per_s": n_total / per,
+                "note": "cvg_timestep: deep kernel + advance (T += tend_T, q += tend_q) + check_finite per step, "
+                        "state resident in HBM; (t(42 steps) - t(2 steps)) / 40, wall clock incl. the per-step "
+                        "divergence check"}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_baseline(s, T, q, thr, args.variant)
@@ -416,6 +433,7 @@ def run_gpu_arm(args):
                                    "untriggered groups (side stream, concurrent)"},
         "gpu_launches": 3 * K,
         "e2e": e2e,
+        "feedback_loop": loop,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
@@ -440,6 +458,7 @@ def main():
     ap.add_argument("--partition", default="balanced", choices=["balanced", "naive"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-loop", action="store_true", help="skip the feedback-loop measurement")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
