@@ -107,6 +107,9 @@ def ref_lib():
                                        C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.POINTER(C.c_double), C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_packed_bytes.restype = C.c_int
+        L.ref_packed_bytes.argtypes = [C.c_longlong, C.c_int, C.c_int, C.POINTER(C.c_longlong),
+                                       C.POINTER(C.c_longlong)]
         L.ref_error_growth.restype = C.c_int
         L.ref_error_growth.argtypes = [C.c_int, C.c_longlong, C.c_int, _dp, _dp, _dp, C.c_int, C.c_int,
                                        C.c_double, C.c_double, C.c_int, C.c_int, _dp, _dp,
@@ -247,3 +250,12 @@ def ref_error_growth(kernel: str, s, T, q, base_variant=EXACT, mod_variant=EXACT
                                           C.byref(env), C.byref(worst), C.byref(fs))
     g.envelope_ok, g.worst_ratio, g.fail_step = bool(env.value), worst.value, fs.value
     return g
+
+
+def ref_packed_bytes(nd, L, send_scalars=True):
+    """(bytes_in, bytes_out) of the reference's device staging for nd columns
+    (hetero.cpp pack(), HeteroMetrics semantics)."""
+    bi, bo = C.c_longlong(), C.c_longlong()
+    if ref_lib().ref_packed_bytes(nd, L, int(send_scalars), C.byref(bi), C.byref(bo)) != 0:
+        raise RuntimeError("ref_packed_bytes failed")
+    return bi.value, bo.value

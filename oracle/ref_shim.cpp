@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "errors.hpp"
+#include "hetero.hpp"
 #include "physics.hpp"
 #include "sched.hpp"
 #include "validate.hpp"
@@ -174,6 +175,39 @@ int ref_run_parallel(void* h, int kernel, int variant, double thr, double tol,
     return 0;
   } catch (const KernelError&) {
     return 3;
+  } catch (...) {
+    return 1;
+  }
+}
+
+// ---- staging byte accounting (hetero.cpp:178-201, :268-312, :336-374) -----
+//
+// The reference's device staging packs T, q, s (+ the 4-double option block
+// "env" unless scalars are resident) into one 8-byte-aligned payload, and the
+// outputs tend_T, tend_q, precip, work_units, exited into another; bytes_in /
+// bytes_out are the payload sizes (HeteroMetrics, hetero.hpp:120-131).  This
+// reproduces them with the reference's own pack() for nd device columns.
+int ref_packed_bytes(long long nd, int L, int send_scalars, long long* bytes_in, long long* bytes_out) {
+  try {
+    std::vector<double> tl(static_cast<size_t>(nd * L)), ql(tl.size()), sl(static_cast<size_t>(nd));
+    double env[4] = {0.5, 1e-12, 100.0, 0.0};
+    std::vector<NamedArray> in = {
+        {"T", tl.data(), tl.size() * sizeof(double)},
+        {"q", ql.data(), ql.size() * sizeof(double)},
+        {"s", sl.data(), sl.size() * sizeof(double)},
+    };
+    if (send_scalars) in.push_back({"env", env, sizeof(env)});
+    *bytes_in = static_cast<long long>(pack(in).payload.size());
+    std::vector<double> pr(static_cast<size_t>(nd));
+    std::vector<long long> wu(static_cast<size_t>(nd));
+    std::vector<std::uint8_t> ex(static_cast<size_t>(nd));
+    *bytes_out = static_cast<long long>(pack({{"tend_T", tl.data(), tl.size() * sizeof(double)},
+                                              {"tend_q", ql.data(), ql.size() * sizeof(double)},
+                                              {"precip", pr.data(), pr.size() * sizeof(double)},
+                                              {"work_units", wu.data(), wu.size() * sizeof(long long)},
+                                              {"exited", ex.data(), ex.size()}})
+                                             .payload.size());
+    return 0;
   } catch (...) {
     return 1;
   }

@@ -271,3 +271,18 @@ def test_group_tails(ctx, n):
         deep, sh = ctx.convect(s, T, q)
         both_close(deep, O.convection("deep", s, T, q))
         both_close(sh, O.convection("shallow", s, T, q))
+
+
+@pytest.mark.parametrize("kernels,nk", [(P.DEEP, 1), (P.SHALLOW, 1), (P.BOTH, 2)])
+def test_staging_bytes_follow_reference_pack(ctx, kernels, nk):
+    """Host-buffer calls report the staging bytes of the reference's packed
+    device transfer (hetero.cpp pack(), HeteroMetrics bytes_in / bytes_out):
+    inputs T, q, s with the option scalars resident (kernel parameters), and
+    tend_T, tend_q, precip, work_units, exited per kernel."""
+    if not O.ref_available():
+        pytest.skip("reference build missing")
+    s, T, q = G.make_config("c1", n=3333, seed=2)
+    ctx.convect(s, T, q, kernels=kernels)
+    st = ctx.last_stats
+    bi, bo = O.ref_packed_bytes(s.size, T.shape[0], send_scalars=False)
+    assert st.h2d_bytes == bi and st.d2h_bytes == nk * bo

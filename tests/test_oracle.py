@@ -241,3 +241,14 @@ def test_reference_error_growth_c11():
         assert g.status == 0 and g.envelope_ok and g.rms_pert[-1] > 0.0
     g = O.ref_error_growth("deep", s, T, q, O.EXACT, O.EXACT, 10)
     assert (g.rms_mod == 0.0).all()
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference build missing")
+@pytest.mark.parametrize("nd", [0, 1, 7, 1000])
+def test_reference_packed_bytes_formula(nd):
+    """The staging byte accounting this repo reports (stats h2d/d2h) is the
+    reference's pack() payload: 8 nd (2L + 1) in (+32 with the option block),
+    16 nd L + 17 nd out per kernel."""
+    L = 30
+    assert O.ref_packed_bytes(nd, L, True) == (8 * nd * (2 * L + 1) + 32, 16 * nd * L + 17 * nd)
+    assert O.ref_packed_bytes(nd, L, False) == (8 * nd * (2 * L + 1), 16 * nd * L + 17 * nd)
