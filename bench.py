@@ -439,6 +439,9 @@ def run_gpu_arm(args):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+        if args.records:   # the reference's pinned BenchRecord CSV (bench.hpp:30-43)
+            from paper_1711_00289_b200 import records
+            records.append_records(args.records, [records.run_gpu_record(line)])
     ctx.close()
     if dist:
         dist.barrier()
@@ -459,6 +462,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-loop", action="store_true", help="skip the feedback-loop measurement")
+    ap.add_argument("--records", default=None,
+                    help="append a run-gpu BenchRecord row (reference CSV schema) to this file")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -110,6 +110,8 @@ def ref_lib():
         L.ref_packed_bytes.restype = C.c_int
         L.ref_packed_bytes.argtypes = [C.c_longlong, C.c_int, C.c_int, C.POINTER(C.c_longlong),
                                        C.POINTER(C.c_longlong)]
+        L.ref_records_roundtrip.restype = C.c_int
+        L.ref_records_roundtrip.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.c_char_p, C.c_int]
         L.ref_error_growth.restype = C.c_int
         L.ref_error_growth.argtypes = [C.c_int, C.c_longlong, C.c_int, _dp, _dp, _dp, C.c_int, C.c_int,
                                        C.c_double, C.c_double, C.c_int, C.c_int, _dp, _dp,
@@ -259,3 +261,12 @@ def ref_packed_bytes(nd, L, send_scalars=True):
     if ref_lib().ref_packed_bytes(nd, L, int(send_scalars), C.byref(bi), C.byref(bo)) != 0:
         raise RuntimeError("ref_packed_bytes failed")
     return bi.value, bo.value
+
+
+def ref_records_roundtrip(csv: str):
+    """(status, n_records, text): the reference's records_from_csv then
+    records_to_csv (bench.cpp:454-525); status 0 ok, 2 ConfigError."""
+    n = C.c_int(0)
+    buf = C.create_string_buffer(1 << 16)
+    st = ref_lib().ref_records_roundtrip(csv.encode(), C.byref(n), buf, len(buf))
+    return st, n.value, buf.value.decode()

@@ -18,6 +18,7 @@
 #include <exception>
 #include <vector>
 
+#include "bench.hpp"
 #include "errors.hpp"
 #include "hetero.hpp"
 #include "physics.hpp"
@@ -208,6 +209,32 @@ int ref_packed_bytes(long long nd, int L, int send_scalars, long long* bytes_in,
                                               {"exited", ex.data(), ex.size()}})
                                              .payload.size());
     return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
+// ---- BenchRecord CSV (bench.cpp:454-525) ------------------------------------
+//
+// Parses a records CSV with the reference's own records_from_csv and writes
+// it back with records_to_csv: 0 ok (*n_records set, out receives the
+// re-serialised CSV when it fits), 2 ConfigError (message in out), 1 other.
+int ref_records_roundtrip(const char* csv, int* n_records, char* out, int out_len) {
+  try {
+    const std::vector<BenchRecord> recs = records_from_csv(csv);
+    *n_records = static_cast<int>(recs.size());
+    const std::string s = records_to_csv(recs);
+    if (out && out_len > 0) {
+      std::strncpy(out, s.c_str(), static_cast<size_t>(out_len - 1));
+      out[out_len - 1] = 0;
+    }
+    return 0;
+  } catch (const ConfigError& e) {
+    if (out && out_len > 0) {
+      std::strncpy(out, e.what(), static_cast<size_t>(out_len - 1));
+      out[out_len - 1] = 0;
+    }
+    return 2;
   } catch (...) {
     return 1;
   }
