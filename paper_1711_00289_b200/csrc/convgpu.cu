@@ -244,7 +244,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     // deep block size: kDeepWarpsOverlap leaves each SM room for three
     // shallow blocks beside the deep block; kDeepWarps when deep runs alone
     const int nw = ctx->deep_warps > 0 ? ctx->deep_warps : (ov ? cvg::kDeepWarpsOverlap : cvg::kDeepWarps);
-    if (false) {    } else if (a.L <= 32) {
+    if (a.L <= 32) {
       if (nw == 16) launch_deep_t<VAR, true, 16>(ctx, a, st);
       else if (nw == 20) launch_deep_t<VAR, true, 20>(ctx, a, st);
       else if (nw == 14) launch_deep_t<VAR, true, 14>(ctx, a, st);
