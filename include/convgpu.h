@@ -81,6 +81,10 @@ typedef struct cvg_options {
  * variant (the default relaxed update of Exact/StrengthReduced differs from
  * it only by rounding noise inside the parity window). */
 #define CVG_FLAG_STRICT 1
+/* cvg_options.flags: no FP32 far phase in the relaxed Newton solve (the far
+ * steps of Exact/StrengthReduced run in FP32 until |resid| <= 0.25, then the
+ * solve continues in FP64). */
+#define CVG_FLAG_NO_FAR32 2
 
 /* Input column block (the SoA form of convproxy::Chunk, physics.hpp:39-43). */
 typedef struct cvg_columns {

@@ -42,18 +42,21 @@ class Variant:
 
 
 FLAG_STRICT = 1
+FLAG_NO_FAR32 = 2
 
 
 class KernelOptions(C.Structure):
     """convproxy::KernelOptions (physics.hpp:68-73), same defaults, plus
-    ``strict``: reference rounding in every Newton update (CVG_FLAG_STRICT)."""
+    ``strict``: reference rounding in every Newton update (CVG_FLAG_STRICT);
+    ``far32=False``: no FP32 far phase in the relaxed solve (CVG_FLAG_NO_FAR32)."""
     _fields_ = [("variant", C.c_int), ("activity_threshold", C.c_double),
                 ("newton_tol", C.c_double), ("newton_max_iter", C.c_int), ("flags", C.c_int)]
 
     def __init__(self, variant=Variant.EXACT, activity_threshold=0.5, newton_tol=1e-12,
-                 newton_max_iter=100, strict=False):
+                 newton_max_iter=100, strict=False, far32=True):
         super().__init__(int(variant), float(activity_threshold), float(newton_tol),
-                         int(newton_max_iter), FLAG_STRICT if strict else 0)
+                         int(newton_max_iter),
+                         (FLAG_STRICT if strict else 0) | (0 if far32 else FLAG_NO_FAR32))
 
     def __repr__(self):
         return (f"KernelOptions(variant={self.variant}, activity_threshold={self.activity_threshold},"

@@ -162,6 +162,7 @@ struct cvg_context {
   bool fused = false;      // CVG_FUSED: shallow tiles inside the deep kernel (L <= 32)
   int shallow_minb = 8;    // CVG_SHALLOW_MINB: shallow blocks per SM the register budget targets (8, 12, 16)
   bool strict = false;     // CVG_STRICT: reference rounding in every Newton update (all variants)
+  bool far32 = true;       // CVG_FAR32: FP32 far phase of the relaxed Newton solve
   long long chunk_cols = kChunkCols;  // CVG_CHUNK_COLS: host-call pipeline chunk
   int slots = 3;                      // CVG_SLOTS: workspaces used by host-buffer calls (1..kSlots)
   const char* trace_path = nullptr;   // CVG_TRACE: per-block (kernel, smid, start, end)
@@ -199,7 +200,7 @@ bool valid_outputs(const cvg_outputs* o, long long n, std::string* why) {
 
 bool valid_options(const cvg_options* o, std::string* why) {
   if (o->variant < 0 || o->variant > 2) { *why = "unknown variant"; return false; }
-  if (o->flags & ~CVG_FLAG_STRICT) { *why = "unknown flags"; return false; }
+  if (o->flags & ~(CVG_FLAG_STRICT | CVG_FLAG_NO_FAR32)) { *why = "unknown flags"; return false; }
   return true;
 }
 
@@ -323,6 +324,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.L = L;
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
     a.relaxed = !strict;
+    a.far32 = !strict && ctx->far32 && (o->flags & CVG_FLAG_NO_FAR32) == 0;
   }
   a.exp_tab = ctx->exp_tab.p;
   if (pe) CVG_CUDA(cudaEventRecord(pe[1], st));
@@ -463,6 +465,7 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     ctx->num_sms = prop.multiProcessorCount;
     if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
     if (const char* e = getenv("CVG_STRICT")) ctx->strict = atoi(e) != 0;
+    if (const char* e = getenv("CVG_FAR32")) ctx->far32 = atoi(e) != 0;
     if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
     if (const char* e = getenv("CVG_FUSED")) ctx->fused = atoi(e) != 0;
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);

@@ -144,6 +144,7 @@ struct DeepArgs {
   int L;                  // levels
   bool fast_div_ok;       // newton_tol >= 2^-500
   bool relaxed;           // relaxed-rounding Newton update allowed (colmath.cuh)
+  bool far32;             // FP32 far phase allowed (relaxed only; colmath.cuh)
 };
 
 // Deep-kernel lanes read a lane-private copy of the exp table (see
@@ -238,6 +239,33 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
     CVG_PCLK(pl0);
     int left = maxit + 1;   // updates still allowed (the loop may take one
                             // more than maxit; newton_finish then fails it)
+    if (a.far32 && far32_ok(ye, guess, tol) && far32_ok(yp, guess, tol)) {
+      // FP32 far phase (colmath.cuh): both solves while both |h| > kFar32H,
+      // then exp and h re-evaluated in FP64 at the FP32 iterates
+      float fte = (float)guess, ftp = fte, fee = (float)e0, fep = fee;
+      float fhe = (float)he, fhp = (float)hp;
+      const float fye = (float)ye, fyp = (float)yp;
+      while (left > 0 && fminf(fabsf(fhe), fabsf(fhp)) > kFar32H) {
+        newton_far32_step(fte, fee, fhe, fye);
+        newton_far32_step(ftp, fep, fhp, fyp);
+        --left;
+      }
+      te = fte;
+      tp = ftp;
+      ee = exp_relaxed1(kRC, te, tab1_addr);
+      ep = exp_relaxed1(kRC, tp, tab1_addr);
+      he = fma(kMC.c001, te, ee - ye);
+      hp = fma(kMC.c001, tp, ep - yp);
+      if (!(he > 0.0 && hp > 0.0)) {
+        // left of a root (not expected: the switch happens O(1) away from
+        // it): redo both solves from the guess with the FP64 update
+        te = tp = guess;
+        ee = ep = e0;
+        he = sub(c0, ye);
+        hp = sub(c0, yp);
+        left = maxit + 1;
+      }
+    }
     if (left > 0) do {
       if (abs_le_either(he, hp, tol)) break;
       newton_relaxed_step(te, ee, he, ye, tab1_addr);

@@ -8,7 +8,12 @@ Parity rule (BASELINE.json north_star), written here:
   * work_units: exact, except deep columns whose Newton residual came within
     1e-3 relative of newton_tol (the glibc-vs-device exp classifier); for the
     ApproxTranscendental variant exact everywhere (pure IEEE arithmetic);
-  * fp64 fields: within 1e-10 relative or 1e-14 absolute, every column.
+  * fp64 fields: within 1e-10 relative or 1e-14 absolute, every column --
+    except that in a deep column whose work_units flipped inside the margin
+    class the absolute bound is 1e-12: one Newton update more or less moves
+    that solve's root by |resid| / f' <= 1e-12 / 0.07, which shifts tend_T by
+    0.04 dr and precip by q dr (measured worst: 2.4e-13 on a precip of 1e-4,
+    full c5_95 grid, column 644381, with or without the FP32 far phase).
 """
 import glob
 import os
@@ -23,6 +28,7 @@ from paper_1711_00289_b200 import gridgen as G
 pytestmark = pytest.mark.gpu
 
 REL, ABS = 1e-10, 1e-14
+ABS_FLIPPED = 1e-12
 NEWTON_MARGIN = 1e-3
 PRED_MARGIN = 1e-9
 GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
@@ -37,6 +43,9 @@ def check(got: P.ColumnOutputs, want, kernel: str, margin=None, bitexact_work=Fa
         exempt = margin < PRED_MARGIN
     assert np.array_equal(got.exited_early[~exempt], g("exited")[~exempt]), f"{kernel}: exit/trigger flags differ"
     flip = got.work_units != g("work")
+    abs_col = np.full(flip.shape, ABS)
+    if kernel == "deep" and margin is not None and not bitexact_work:
+        abs_col[flip & (margin < NEWTON_MARGIN)] = ABS_FLIPPED
     if bitexact_work:
         assert not flip.any(), f"{kernel}: work_units differ in {int(flip.sum())} columns"
     elif kernel == "deep" and margin is not None:
@@ -46,7 +55,7 @@ def check(got: P.ColumnOutputs, want, kernel: str, margin=None, bitexact_work=Fa
         assert not (flip & ~exempt).any(), "shallow: phase counts differ"
     for f in ("tend_T", "tend_q", "precip"):
         a, b = getattr(got, f), g(f)
-        ok = np.abs(a - b) <= np.maximum(REL * np.abs(b), ABS)
+        ok = np.abs(a - b) <= np.maximum(REL * np.abs(b), abs_col)
         assert ok.all(), f"{kernel}.{f}: {int((~ok).sum())} values outside tolerance, max |d| {np.max(np.abs(a - b))}"
     return int(flip.sum())
 
@@ -196,3 +205,34 @@ def test_relaxed_guard_falls_back_for_tight_tolerance(ctx, strict_ctx):
     b, _ = strict_ctx.convect(s, T, q, o)
     for f in ("tend_T", "tend_q", "precip", "work_units", "exited_early"):
         assert np.array_equal(getattr(a, f), getattr(b, f))
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5_95"])
+def test_far32_full_grid_every_column(ctx, cfg):
+    """The FP32 far phase of the relaxed Newton solve (default for Exact;
+    colmath.cuh newton_far32_step) against the oracle on EVERY column of the
+    full 884,736-column grid: flags exact, work_units exact outside the
+    Newton-margin class, fp64 fields within tolerance."""
+    s, T, q = G.make_config(cfg, seed=42)
+    deep, _ = ctx.convect(s, T, q, P.KernelOptions(), kernels=P.DEEP)
+    od = O.convection("deep", s, T, q)
+    flips = check(deep, od, "deep")
+    assert flips <= 1e-3 * int((s > 0.5).sum())   # 74 at c4 (all inside the margin class)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("cfg,kw", [("c2", {}), ("c3", {"shape": (96, 144)}), ("c5_95", {"shape": (64, 96)})],
+                         ids=["c2", "c3", "c5_95"])
+def test_far32_against_fp64_update(ctx, cfg, kw, variant):
+    """far32 on vs off (CVG_FLAG_NO_FAR32): both match the oracle, and each
+    other up to rounding noise (work equal outside the margin class)."""
+    s, T, q = G.make_config(cfg, seed=21, **kw)
+    thr = G.config_threshold(cfg)
+    oo = O.Options(variant=variant, activity_threshold=thr)
+    od = O.convection("deep", s, T, q, oo)
+    a, _ = ctx.convect(s, T, q, P.KernelOptions(variant=variant, activity_threshold=thr))
+    b, _ = ctx.convect(s, T, q, P.KernelOptions(variant=variant, activity_threshold=thr, far32=False))
+    check(a, od, "deep")
+    check(b, od, "deep")
+    check(a, {"tend_T": b.tend_T, "tend_q": b.tend_q, "precip": b.precip, "work": b.work_units,
+              "exited": b.exited_early}, "deep", margin=od.margin)
