@@ -78,4 +78,9 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// 256-bit global store (sm_100: STG.E.ENL2.256); p 32-byte aligned.
+__device__ __forceinline__ void st_global_v4f64(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 }  // namespace cvg

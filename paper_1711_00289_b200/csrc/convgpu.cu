@@ -204,6 +204,22 @@ bool valid_options(const cvg_options* o, std::string* why) {
   return true;
 }
 
+// Hot-path window of the deep Newton solve (colmath.cuh in_far_window): the
+// high-word bound lim of the targets y in [0.25, 16) for which the FP32 far
+// phase and the relaxed update are both admissible -- relaxed_ok(y, tol)
+// holds iff the exponent of y is <= that of tol + 40 (y >= 1) or tol >=
+// 2^-40 (y < 1), and the far phase needs tol <= 1e-6.  Empty window (lim =
+// hi(0.25)) when the far phase is off.
+static int far_window_limit(double tol, bool enabled) {
+  if (!enabled || !(tol <= 1e-6) || !(tol >= 0x1.0p-40)) return cvg::kFarWindowLo;
+  unsigned long long bits;
+  memcpy(&bits, &tol, sizeof bits);
+  const int tol_exp = (int)(bits >> 32) & 0x7ff00000;
+  return std::min(cvg::kFarWindowHi, tol_exp + (41 << 20));
+}
+
+static bool aligned32(const void* p) { return ((uintptr_t)p & 31) == 0; }
+
 // Shared memory of one deep block: both exp tables and the per-warp scratch.
 template <int VAR, bool NARROW, int NW, bool FUSED = false, bool SH = true, bool RELAX_SH = false>
 void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st,
@@ -324,7 +340,10 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.L = L;
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
     a.relaxed = !strict;
-    a.far32 = !strict && ctx->far32 && (o->flags & CVG_FLAG_NO_FAR32) == 0;
+    a.far32 = !strict && ctx->far32 && (o->flags & CVG_FLAG_NO_FAR32) == 0 && o->variant != CVG_APPROX_TRANSCENDENTAL;
+    a.y_win = far_window_limit(o->newton_tol, a.far32);
+    a.tree_precip = !strict && o->variant != CVG_APPROX_TRANSCENDENTAL && o->newton_tol >= 0x1.0p-40;
+    a.vec4 = deep->ld % 4 == 0 && aligned32(deep->tend_T) && aligned32(deep->tend_q);
   }
   a.exp_tab = ctx->exp_tab.p;
   if (pe) CVG_CUDA(cudaEventRecord(pe[1], st));

@@ -145,6 +145,9 @@ struct DeepArgs {
   bool fast_div_ok;       // newton_tol >= 2^-500
   bool relaxed;           // relaxed-rounding Newton update allowed (colmath.cuh)
   bool far32;             // FP32 far phase allowed (relaxed only; colmath.cuh)
+  int y_win;              // far_window_limit(): hi-word bound of the hot path's targets
+  bool tree_precip;       // precip summed as a warp tree (relaxed path; else k order)
+  bool vec4;              // outputs 32-byte aligned with ld_out % 4 == 0 (group stores)
 };
 
 // Deep-kernel lanes read a lane-private copy of the exp table (see
@@ -223,25 +226,23 @@ template <int VAR>
 __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2* tab, unsigned tab1_addr,
                                                long long col,
                                                int k, double ye, double yp, double guess, double e0,
-                                               double c0, double& re, double& rp, int& work) {
+                                               double c0, bool col_far, double& re, double& rp, int& work) {
   const double kBig = 0x1.0p490;
   double te = guess, ee = e0, he = sub(c0, ye);
   double tp = guess, ep = e0, hp = sub(c0, yp);
   int it = 0;
-  const bool inputs_ok = is_finite(ye) && is_finite(yp);
-  const bool fast_ok = inputs_ok && a.fast_div_ok && ye > -60.0 && yp > -60.0 && ye < kBig &&
-                       yp < kBig && he > 0.0 && hp > 0.0 && exp_fast_ok(mul(kMC.c005, guess));
-  if (VAR != kVarApprox && fast_ok && a.relaxed && relaxed_ok(ye, a.tol) && relaxed_ok(yp, a.tol)) {
-    // relaxed update (colmath.cuh): same iteration and stop test, rounding
-    // noise only; the exact sequence below is the one the reference runs
+  const int maxit = a.maxit;
+  if (VAR != kVarApprox && col_far && in_far_window(ye, a.y_win) && in_far_window(yp, a.y_win) &&
+      min(hi_word(he), hi_word(hp)) > 0) {
+    // Hot path.  The window (host-computed, far_window_limit) guarantees
+    // the fast-loop precondition P and relaxed_ok for both targets; the
+    // guess is right of both roots (residuals > 0).  FP32 far phase
+    // (colmath.cuh) while both |h| > kFar32H, then exp and h re-evaluated
+    // in FP64 at the FP32 iterates and the relaxed FP64 update to the end.
     const double tol = a.tol;
-    const int maxit = a.maxit;
-    CVG_PCLK(pl0);
     int left = maxit + 1;   // updates still allowed (the loop may take one
                             // more than maxit; newton_finish then fails it)
-    if (a.far32 && far32_ok(ye, guess, tol) && far32_ok(yp, guess, tol)) {
-      // FP32 far phase (colmath.cuh): both solves while both |h| > kFar32H,
-      // then exp and h re-evaluated in FP64 at the FP32 iterates
+    {
       float fte = (float)guess, ftp = fte, fee = (float)e0, fep = fee;
       float fhe = (float)he, fhp = (float)hp;
       const float fye = (float)ye, fyp = (float)yp;
@@ -252,20 +253,21 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
       }
       te = fte;
       tp = ftp;
-      ee = exp_relaxed1(kRC, te, tab1_addr);
-      ep = exp_relaxed1(kRC, tp, tab1_addr);
-      he = fma(kMC.c001, te, ee - ye);
-      hp = fma(kMC.c001, tp, ep - yp);
-      if (!(he > 0.0 && hp > 0.0)) {
-        // left of a root (not expected: the switch happens O(1) away from
-        // it): redo both solves from the guess with the FP64 update
-        te = tp = guess;
-        ee = ep = e0;
-        he = sub(c0, ye);
-        hp = sub(c0, yp);
-        left = maxit + 1;
-      }
     }
+    ee = exp_relaxed1(kRC, te, tab1_addr);
+    ep = exp_relaxed1(kRC, tp, tab1_addr);
+    he = fma(kMC.c001, te, ee - ye);
+    hp = fma(kMC.c001, tp, ep - yp);
+    if (min(hi_word(he), hi_word(hp)) <= 0) {
+      // left of a root (not expected: the switch happens O(1) away from
+      // it): redo both solves from the guess with the FP64 update
+      te = tp = guess;
+      ee = ep = e0;
+      he = sub(c0, ye);
+      hp = sub(c0, yp);
+      left = maxit + 1;
+    }
+    CVG_PCLK(pl0);
     if (left > 0) do {
       if (abs_le_either(he, hp, tol)) break;
       newton_relaxed_step(te, ee, he, ye, tab1_addr);
@@ -277,9 +279,30 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
       const int lane = threadIdx.x & 31;
       CVG_PACC(4, pl0, pl1);   // relaxed Newton loop
     }
+    int ie = it, ip = it;
+    bool ok = newton_finish<VAR>(a, tab, col, k, ye, te, ee, he, ie);
+    if (!newton_finish<VAR>(a, tab, col, a.L + k, yp, tp, ep, hp, ip)) ok = false;
+    re = te;
+    rp = tp;
+    work = ie + ip;
+    return ok;
+  }
+  const bool inputs_ok = is_finite(ye) && is_finite(yp);
+  const bool fast_ok = inputs_ok && a.fast_div_ok && ye > -60.0 && yp > -60.0 && ye < kBig &&
+                       yp < kBig && he > 0.0 && hp > 0.0 && exp_fast_ok(mul(kMC.c005, guess));
+  if (VAR != kVarApprox && fast_ok && a.relaxed && relaxed_ok(ye, a.tol) && relaxed_ok(yp, a.tol)) {
+    // relaxed update (colmath.cuh): same iteration and stop test, rounding
+    // noise only; the exact sequence below is the one the reference runs
+    const double tol = a.tol;
+    int left = maxit + 1;
+    if (left > 0) do {
+      if (abs_le_either(he, hp, tol)) break;
+      newton_relaxed_step(te, ee, he, ye, tab1_addr);
+      newton_relaxed_step(tp, ep, hp, yp, tab1_addr);
+    } while (--left != 0);
+    it = maxit + 1 - max(left, 0);
   } else if (fast_ok) {
     const double tol = a.tol;
-    const int maxit = a.maxit;
     while (it <= maxit) {
       if (abs_le(he, tol) || abs_le(hp, tol)) break;   // tol >= 2^-500 here
       te = sub(te, div_fast(he, add(mul(kMC.c005, ee), kMC.c001)));
@@ -407,12 +430,17 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
   // register scoreboard shared with the column's other loads
   int buf = 0;
   const unsigned st_addr = opaque_u32(smem_u32(s_warp + lane));
+  // this lane's level rows (lane < L)
+  const double* T_row = a.T + (long long)min(lane, L - 1) * a.ld_in;
+  const double* q_row = a.q + (long long)min(lane, L - 1) * a.ld_in;
+  double* outT_row = a.tend_T + (long long)min(lane, L - 1) * a.ld_out;
+  double* outQ_row = a.tend_q + (long long)min(lane, L - 1) * a.ld_out;
   auto stage = [&](long long cc, int b) {
     const unsigned d = st_addr + b * 768;
     cp_async8_u32(d, a.s + cc);
     if (lane < L) {
-      cp_async8_u32(d + 256, a.T + (long long)lane * a.ld_in + cc);
-      cp_async8_u32(d + 512, a.q + (long long)lane * a.ld_in + cc);
+      cp_async8_u32(d + 256, T_row + cc);
+      cp_async8_u32(d + 512, q_row + cc);
     }
     cp_async_commit();
   };
@@ -447,10 +475,12 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     const double rho = add(1.0, mul(kMC.c005, sc));
     const double e0 = deep_exp<VAR>(mul(kMC.c005, guess), s_tab);
     const double c0 = add(e0, mul(kMC.c001, guess));
+    const bool col_far = guess < 1190.0;   // far phase: exp(0.05 guess) < 2^86
     CVG_PCLK(ph1);
     const long long col = a.first_col + c;
     int wl = 0;
     bool ok_all = true;
+    double term_l = 0.0;   // tree_precip: this lane's precipitation term
     // NARROW (L <= 32): one level per lane, its (T, q) staged; wide columns
     // loop over levels lane, lane + 32, ... with plain loads
     for (int k = lane; k < L; k += 32) {
@@ -479,7 +509,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       double re = 0.0, rp = 0.0;
       int w = 0;
       double term = 0.0, tT = 0.0, tq = 0.0;
-      if (deep_lane_pair<VAR>(a, s_tab, tab1_addr, col, k, ye, yp, guess, e0, c0, re, rp, w)) {
+      if (deep_lane_pair<VAR>(a, s_tab, tab1_addr, col, k, ye, yp, guess, e0, c0, col_far, re, rp, w)) {
         // physics.cpp:151-152 / :159-161
         double sin_a, sin_b;
         sin2_cw(add(mul(6.0, T), mul(50.0, q)), mul(3.0, rp), sin_a, sin_b);
@@ -492,7 +522,8 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       if (NARROW) {
         s_outT[i * 32 + k] = tT;
         s_outQ[i * 32 + k] = tq;
-        s_term[i * 32 + k] = term;
+        if (!a.tree_precip) s_term[i * 32 + k] = term;
+        else term_l = term;
       } else {
         a.tend_T[(long long)k * a.ld_out + c] = tT;
         a.tend_q[(long long)k * a.ld_out + c] = tq;
@@ -503,6 +534,13 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     CVG_PCLK(ph3);
     const int wsum = __reduce_add_sync(0xffffffffu, wl);
     const bool ok = __all_sync(0xffffffffu, ok_all);
+    if (NARROW && a.tree_precip) {
+      // relaxed path: precip as a fixed-shape warp tree (terms >= 0, so
+      // within 30 ulp of the reference's k-order sum, physics.cpp:161)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) term_l = add(term_l, __shfl_xor_sync(0xffffffffu, term_l, o));
+      if (lane == 0) s_gpr[i] = term_l;
+    }
     if (lane == 0) {
       s_gwork[i] = wsum;
       s_gok[i] = ok;
@@ -520,13 +558,27 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       // zeros for its untriggered columns (physics.cpp:89-97)
       const long long c0g = g * kGroupCols;
       if (NARROW) {
-        for (int r = lane; r < kGroupCols * L; r += 32) {
-          const int k = r / kGroupCols, ii = r % kGroupCols;
-          const long long cc = c0g + ii;
-          if (cc < a.n) {
+        // lane k writes row k of the group: 4 columns = one 32-byte sector
+        if (lane < L) {
+          double vT[kGroupCols], vQ[kGroupCols];
+#pragma unroll
+          for (int ii = 0; ii < kGroupCols; ++ii) {
             const bool trig = (m >> ii) & 1u;
-            a.tend_T[(long long)k * a.ld_out + cc] = trig ? s_outT[ii * 32 + k] : 0.0;
-            a.tend_q[(long long)k * a.ld_out + cc] = trig ? s_outQ[ii * 32 + k] : 0.0;
+            vT[ii] = trig ? s_outT[ii * 32 + lane] : 0.0;
+            vQ[ii] = trig ? s_outQ[ii * 32 + lane] : 0.0;
+          }
+          double* pT = outT_row + c0g;
+          double* pQ = outQ_row + c0g;
+          if (a.vec4 && c0g + kGroupCols <= a.n) {
+            st_global_v4f64(pT, vT[0], vT[1], vT[2], vT[3]);
+            st_global_v4f64(pQ, vQ[0], vQ[1], vQ[2], vQ[3]);
+          } else {
+#pragma unroll
+            for (int ii = 0; ii < kGroupCols; ++ii)
+              if (c0g + ii < a.n) {
+                pT[ii] = vT[ii];
+                pQ[ii] = vQ[ii];
+              }
           }
         }
       } else {
@@ -543,7 +595,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
         const long long cc = c0g + lane;
         if ((m >> lane) & 1u) {
           double pr = 0.0;
-          if (NARROW) {   // ordered k sum, physics.cpp:161
+          if (NARROW && !a.tree_precip) {   // ordered k sum, physics.cpp:161
             const double* tt = s_term + lane * 32;
             for (int kk = 0; kk < L; ++kk) pr = add(pr, tt[kk]);
           } else {
