@@ -253,19 +253,33 @@ def run_gpu_arm(args):
     # partition: contiguous ranges balanced by estimated cost (multigpu.py)
     from paper_1711_00289_b200 import multigpu
     hbm_gbs, hbm_src = measured_peaks()
-    bounds = multigpu.rank_bounds(s, thr, ws, args.partition, L, hbm_gbs)
-    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    if args.slice:
+        # diagnostic: one rank's share of a W-way partition, run alone on this GPU
+        pr, pw = (int(x) for x in args.slice.split("/"))
+        bounds = multigpu.rank_bounds(s, thr, pw, args.partition, L, hbm_gbs)
+        lo, hi = int(bounds[pr]), int(bounds[pr + 1])
+    else:
+        bounds = multigpu.rank_bounds(s, thr, ws, args.partition, L, hbm_gbs)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     n = hi - lo
     s_r, T_r, q_r = s[lo:hi], np.ascontiguousarray(T[:, lo:hi]), np.ascontiguousarray(q[:, lo:hi])
 
     ctx = P.Context(local)
+    # level rows pitched to a multiple of 32 columns (256-byte aligned rows)
+    ldp = (n + 31) // 32 * 32
+
+    def rows(a=None):
+        t = torch.empty((L, ldp), dtype=torch.float64, device=dev)[:, :n]
+        if a is not None:
+            t.copy_(torch.from_numpy(a))
+        return t
+
     ds = torch.from_numpy(s_r).to(dev)
-    dT = torch.from_numpy(T_r).to(dev)
-    dq = torch.from_numpy(q_r).to(dev)
+    dT = rows(T_r)
+    dq = rows(q_r)
 
     def alloc_out():
-        return (torch.empty((L, n), dtype=torch.float64, device=dev),
-                torch.empty((L, n), dtype=torch.float64, device=dev),
+        return (rows(), rows(),
                 torch.empty(n, dtype=torch.float64, device=dev),
                 torch.empty(n, dtype=torch.int64, device=dev),
                 torch.empty(n, dtype=torch.uint8, device=dev))
@@ -287,7 +301,6 @@ def run_gpu_arm(args):
     K = args.steps
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    ctx.profile_begin(K)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -302,6 +315,23 @@ def run_gpu_arm(args):
     if dist:
         dist.barrier()
     ms_local = ev0.elapsed_time(ev1)
+    ctx.check(stream)
+    if os.environ.get("BENCH_DEBUG"):
+        print(f"debug: lo={lo} hi={hi} n={n} ms/step={ms_local / K:.4f}", file=sys.stderr)
+        for rep in range(3):
+            ev0.record(stream)
+            for _ in range(K):
+                step()
+            ev1.record(stream)
+            stream.synchronize()
+            print(f"debug: rep {rep} ms/step={ev0.elapsed_time(ev1) / K:.4f}", file=sys.stderr)
+    # per-kernel breakdown from a separate, untimed pass with event pairs
+    # between the kernels (kept out of the timed region: the extra event
+    # records cost a few us per step, which shows at small per-GPU shares)
+    ctx.profile_begin(K)
+    for _ in range(K):
+        step()
+    stream.synchronize()
     kern = ctx.profile_end(K)  # [K][3] trigger, deep, shallow (ms)
     ctx.check(stream)
 
@@ -316,7 +346,7 @@ def run_gpu_arm(args):
     else:
         ms_total, n_trig = ms_local, n_trig_local
     ms_step = ms_total / K
-    value = n_total * K / (ms_total * 1e-3)
+    value = (n if args.slice else n_total) * K / (ms_total * 1e-3)
 
     # model FLOPs from this rank's outputs (work_units / exit flags match the oracle)
     dw = deep_o[3].cpu().numpy()
@@ -345,8 +375,15 @@ def run_gpu_arm(args):
             pass
     deep_bytes_alg = trig_r * (8 + 2 * 8 * L + 2 * 8 * L + 8 + 8 + 1)
     bytes_step, per_col, deep_bytes = bytes_model(n, L, trig_r)
-    t_flop = (deep_flops + sh_flops) / (fp64_peak * 1e12)
-    t_hbm = bytes_step / (hbm_gbs * 1e9)
+    # roofline of the whole job per GPU: total FLOPs and bytes over all
+    # ranks, divided over the N GPUs (the slower of the two bounds)
+    tot = torch.tensor([deep_flops + sh_flops, float(bytes_step)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    flops_job, bytes_job = float(tot[0]), float(tot[1])
+    nper = 1 if args.slice else ws
+    t_flop = flops_job / nper / (fp64_peak * 1e12)
+    t_hbm = bytes_job / nper / (hbm_gbs * 1e9)
     t_roof = max(t_flop, t_hbm)
 
     # ---- end-to-end through the public host API (pinned host buffers)
@@ -422,12 +459,13 @@ def run_gpu_arm(args):
                      "flops_per_launch": deep_flops, "ms_per_launch": deep_ms,
                      "algorithmic_bytes_per_launch": deep_bytes_alg,
                      "model": "159*L + 37*U_c FLOP per triggered column (SURVEY 8d), U_c from the step's work_units"},
-        "step_roofline": {"flops": deep_flops + sh_flops, "bytes": bytes_step, "bytes_per_column": per_col,
+        "step_roofline": {"flops": flops_job, "bytes": bytes_job, "bytes_per_column": per_col,
                           "t_fp64_ms": 1e3 * t_flop, "t_hbm_ms": 1e3 * t_hbm,
                           "hbm_peak_gbs": hbm_gbs, "hbm_source": hbm_src,
                           "fp64_peak_tflops": fp64_peak,
                           "bound": "fp64" if t_flop >= t_hbm else "hbm",
-                          "roofline_ms": 1e3 * t_roof, "frac": 1e3 * t_roof / (ms_total / K) if ws == 1 else None},
+                          "roofline_ms": 1e3 * t_roof, "frac": 1e3 * t_roof / (ms_total / K),
+                          "note": "job FLOPs and bytes over all ranks / N GPUs; frac = roofline time / max-over-ranks step time"},
         "kernels_ms": {"trigger_groups": trig_ms, "deep": deep_ms, "shallow_tail_after_deep": sh_ms,
                        "schedule": "trigger/group compaction -> deep (main stream) || shallow + zero-fill of "
                                    "untriggered groups (side stream, concurrent)"},
@@ -465,6 +503,8 @@ def main():
     ap.add_argument("--records", default=None,
                     help="append a run-gpu BenchRecord row (reference CSV schema) to this file")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slice", default=None,
+                    help="diagnostic R/W: time rank R's share of a W-way partition alone on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

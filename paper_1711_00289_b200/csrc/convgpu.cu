@@ -427,23 +427,32 @@ cvg_status guarded(Fn&& body) {
   }
 }
 
-void copy_rows_h2d(double* dst, const double* src, long long n, int L, long long ld, cudaStream_t st) {
-  if (ld == n) {
+// L rows of n doubles: device rows dld apart, host rows hld apart.
+void copy_rows_h2d(double* dst, long long dld, const double* src, long long hld, long long n, int L,
+                   cudaStream_t st) {
+  if (dld == n && hld == n) {
     CVG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * n * L, cudaMemcpyHostToDevice, st));
   } else {
-    CVG_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * n, src, sizeof(double) * ld, sizeof(double) * n, L,
+    CVG_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * dld, src, sizeof(double) * hld, sizeof(double) * n, L,
                                cudaMemcpyHostToDevice, st));
   }
 }
 
-void copy_rows_d2h(double* dst, long long ld, const double* src, long long n, int L, cudaStream_t st) {
-  if (ld == n) {
+void copy_rows_d2h(double* dst, long long hld, const double* src, long long dld, long long n, int L,
+                   cudaStream_t st) {
+  if (dld == n && hld == n) {
     CVG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * n * L, cudaMemcpyDeviceToHost, st));
   } else {
-    CVG_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ld, src, sizeof(double) * n, sizeof(double) * n, L,
+    CVG_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * hld, src, sizeof(double) * dld, sizeof(double) * n, L,
                                cudaMemcpyDeviceToHost, st));
   }
 }
+
+// Row pitch of the library's device staging buffers: a multiple of 32
+// columns, so every level row starts on a 256-byte boundary and a 4-column
+// group is one 32-byte sector in every row (an odd pitch splits the groups
+// and the warps' 256-byte row segments across sectors: measured 25% slower).
+constexpr long long pitch_cols(long long m) { return (m + 31) & ~31LL; }
 
 }  // namespace
 
@@ -639,7 +648,8 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
       CVG_CUDA(cudaStreamWaitEvent(w.stream, ctx->ev_h0, 0));
       const long long c0 = bounds[ci];
       const long long m = bounds[ci + 1] - c0;
-      const size_t mL = (size_t)m * L;
+      const long long mp = pitch_cols(m);
+      const size_t mL = (size_t)mp * L;
       cvg_columns din = *in;
       din.n_columns = m;
       din.first_col = in->first_col + c0;
@@ -648,10 +658,10 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
       } else if (m > 0) {
         w.in_s.ensure(m); w.in_T.ensure(mL); w.in_q.ensure(mL);
         CVG_CUDA(cudaMemcpyAsync(w.in_s.p, in->s + c0, sizeof(double) * m, cudaMemcpyHostToDevice, w.stream));
-        copy_rows_h2d(w.in_T.p, in->T + c0, m, L, in->ld, w.stream);
-        copy_rows_h2d(w.in_q.p, in->q + c0, m, L, in->ld, w.stream);
-        h2d += (long long)(sizeof(double) * (m + 2 * mL));
-        din.s = w.in_s.p; din.T = w.in_T.p; din.q = w.in_q.p; din.ld = m; din.on_device = 1;
+        copy_rows_h2d(w.in_T.p, mp, in->T + c0, in->ld, m, L, w.stream);
+        copy_rows_h2d(w.in_q.p, mp, in->q + c0, in->ld, m, L, w.stream);
+        h2d += (long long)(sizeof(double) * (m + 2 * (size_t)m * L));
+        din.s = w.in_s.p; din.T = w.in_T.p; din.q = w.in_q.p; din.ld = mp; din.on_device = 1;
       }
       auto stage = [&](const cvg_outputs* o, DevBuf<double>& T, DevBuf<double>& q, DevBuf<double>& p,
                        DevBuf<long long>& wk, DevBuf<uint8_t>& x) {
@@ -664,7 +674,7 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
         } else if (m > 0) {
           T.ensure(mL); q.ensure(mL); p.ensure(m); wk.ensure(m); x.ensure(m);
           d.tend_T = T.p; d.tend_q = q.p; d.precip = p.p; d.work_units = wk.p; d.exited_early = x.p;
-          d.ld = m; d.on_device = 1;
+          d.ld = mp; d.on_device = 1;
         }
         return d;
       };
@@ -674,13 +684,13 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
       enqueue(ctx, w, &din, opts, mask, &ddeep, &dsh, w.stream, nullptr);
       auto unstage = [&](const cvg_outputs* o, const cvg_outputs& d) {
         if (o->on_device || m <= 0) return;
-        copy_rows_d2h(o->tend_T + c0, o->ld, d.tend_T, m, L, w.stream);
-        copy_rows_d2h(o->tend_q + c0, o->ld, d.tend_q, m, L, w.stream);
+        copy_rows_d2h(o->tend_T + c0, o->ld, d.tend_T, mp, m, L, w.stream);
+        copy_rows_d2h(o->tend_q + c0, o->ld, d.tend_q, mp, m, L, w.stream);
         CVG_CUDA(cudaMemcpyAsync(o->precip + c0, d.precip, sizeof(double) * m, cudaMemcpyDeviceToHost, w.stream));
         CVG_CUDA(cudaMemcpyAsync(o->work_units + c0, d.work_units, sizeof(long long) * m, cudaMemcpyDeviceToHost,
                                  w.stream));
         CVG_CUDA(cudaMemcpyAsync(o->exited_early + c0, d.exited_early, m, cudaMemcpyDeviceToHost, w.stream));
-        d2h += (long long)(sizeof(double) * (2 * mL + m) + sizeof(long long) * m + m);
+        d2h += (long long)(sizeof(double) * (2 * (size_t)m * L + m) + sizeof(long long) * m + m);
       };
       if (mask & CVG_DEEP) unstage(deep, ddeep);
       if (mask & CVG_SHALLOW) unstage(sh, dsh);

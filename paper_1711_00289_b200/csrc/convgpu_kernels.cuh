@@ -331,6 +331,43 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
   return ok;
 }
 
+// One level (lane) of a triggered column: physics.cpp:140-161 for level k --
+// m = q / rho / rho (physics.hpp:94-96, shared-divisor form of div_rn), the
+// entrainment and precipitation solves (deep_lane_pair), the tendencies and
+// the precipitation term.  Returns false on a numeric failure (outputs 0).
+template <int VAR>
+__device__ __forceinline__ bool deep_level(const DeepArgs& a, const double2* s_tab, unsigned tab1_addr,
+                                           long long col, int k, double sc, double rho, double guess,
+                                           double e0, double c0, bool col_far, double T, double q,
+                                           double& tT, double& tq, double& term, int& w) {
+  const bool reduced = (VAR == kVarReduced);
+  double m_;
+  {
+    const double dv = reduced ? mul(rho, rho) : rho;
+    if (div_operand_ok(dv) && div_operand_ok(q)) {
+      const double ydv = rcp_refined(dv);
+      m_ = div_by(q, dv, ydv);
+      if (!reduced) m_ = div_operand_ok(m_) ? div_by(m_, dv, ydv) : div_rn(m_, dv);
+    } else {
+      m_ = reduced ? div_rn(q, dv) : div_rn(div_rn(q, rho), rho);
+    }
+  }
+  // physics.cpp:147-148 / :156-157
+  const double ye = add(add(1.0, mul(1.0e-3, T)), mul(0.1, m_));
+  const double yp = add(add(add(1.0, mul(8.0e-4, T)), mul(kMC.c005, m_)), mul(0.1, sc));
+  double re = 0.0, rp = 0.0;
+  w = 0;
+  term = tT = tq = 0.0;
+  if (!deep_lane_pair<VAR>(a, s_tab, tab1_addr, col, k, ye, yp, guess, e0, c0, col_far, re, rp, w)) return false;
+  // physics.cpp:151-152 / :159-161
+  double sin_a, sin_b;
+  sin2_cw(add(mul(6.0, T), mul(50.0, q)), mul(3.0, rp), sin_a, sin_b);
+  tT = add(mul(0.02, sub(add(250.0, mul(2.0, re)), T)), mul(0.3, sin_a));
+  tq = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, sin_b)), q));
+  term = mul(q, max0(sub(rp, 4.5)));
+  return true;
+}
+
 // One warp per triggered column, lane k = level k (levels k, k+32, ... when
 // L > 32).  A column's 60 solves share the guess, so their iteration counts
 // agree almost everywhere and the warp runs converged (0.03 mean spread);
@@ -381,7 +418,6 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
                                             unsigned long long* tile_cursor = nullptr, int every = 1) {
   const int L = a.L;
   const long long G = *a.count;
-  const bool reduced = (VAR == kVarReduced);
   // Work distribution: warps claim groups from a global cursor (one atomic
   // per group, a group ahead), so SMs finish together whatever the
   // per-column cost mix.  Software pipeline: a column's (s, T[lane],
@@ -418,10 +454,6 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
   long long jnn = jn < G ? advance(jn) : G;
   long long enn = entry(jnn);
   int groups_done = 0;
-  if (e < 0) {
-    if (FUSED) while (do_tile()) {}
-    return;
-  }
   double* s_outT = s_warp + 2 * 3 * 32;   // NARROW: [4][32]
   double* s_outQ = s_outT + kGroupCols * 32;
   double* s_term = NARROW ? s_outQ + kGroupCols * 32 : s_warp;   // NARROW: [4][32]; wide: [L]
@@ -444,6 +476,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     }
     cp_async_commit();
   };
+  if (e >= 0) {
   long long g = e >> 4;
   unsigned m = (unsigned)(e & 15), rem = m;
   int i = __ffs(rem) - 1;
@@ -492,33 +525,10 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
         T = a.T[(long long)k * a.ld_in + c];
         q = a.q[(long long)k * a.ld_in + c];
       }
-      double m_;  // physics.hpp:94-96 via the shared-divisor form of div_rn
-      {
-        const double dv = reduced ? mul(rho, rho) : rho;
-        if (div_operand_ok(dv) && div_operand_ok(q)) {
-          const double ydv = rcp_refined(dv);
-          m_ = div_by(q, dv, ydv);
-          if (!reduced) m_ = div_operand_ok(m_) ? div_by(m_, dv, ydv) : div_rn(m_, dv);
-        } else {
-          m_ = reduced ? div_rn(q, dv) : div_rn(div_rn(q, rho), rho);
-        }
-      }
-      // physics.cpp:147-148 / :156-157
-      const double ye = add(add(1.0, mul(1.0e-3, T)), mul(0.1, m_));
-      const double yp = add(add(add(1.0, mul(8.0e-4, T)), mul(kMC.c005, m_)), mul(0.1, sc));
-      double re = 0.0, rp = 0.0;
-      int w = 0;
-      double term = 0.0, tT = 0.0, tq = 0.0;
-      if (deep_lane_pair<VAR>(a, s_tab, tab1_addr, col, k, ye, yp, guess, e0, c0, col_far, re, rp, w)) {
-        // physics.cpp:151-152 / :159-161
-        double sin_a, sin_b;
-        sin2_cw(add(mul(6.0, T), mul(50.0, q)), mul(3.0, rp), sin_a, sin_b);
-        tT = add(mul(0.02, sub(add(250.0, mul(2.0, re)), T)), mul(0.3, sin_a));
-        tq = mul(kMC.c005, sub(add(kMC.c001, mul(0.002, sin_b)), q));
-        term = mul(q, max0(sub(rp, 4.5)));
-      } else {
+      double term, tT, tq;
+      int w;
+      if (!deep_level<VAR>(a, s_tab, tab1_addr, col, k, sc, rho, guess, e0, c0, col_far, T, q, tT, tq, term, w))
         ok_all = false;
-      }
       if (NARROW) {
         s_outT[i * 32 + k] = tT;
         s_outQ[i * 32 + k] = tq;
@@ -640,6 +650,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     rem &= rem - 1;
     c = g * kGroupCols + i;
   }
+  }   // e >= 0
   if (FUSED) while (do_tile()) {}
 }
 

@@ -31,11 +31,29 @@ def partition_weights(L: int = 30, hbm_gbs: float = 6558.7, fp64_tflops: float =
 
 def rank_bounds(s, activity_threshold: float, world: int, mode: str = "balanced", L: int = 30,
                 hbm_gbs: float = 6558.7, fp64_tflops: float = 34.0) -> np.ndarray:
-    """world + 1 column offsets; rank r owns [b[r], b[r+1])."""
+    """world + 1 column offsets; rank r owns [b[r], b[r+1]).  Interior
+    boundaries are rounded to multiples of ALIGN columns (a rank's rows then
+    start on 256-byte boundaries and its 4-column groups are whole sectors;
+    the rounding moves at most 16 columns per boundary)."""
     if mode == "naive":
-        return plan_partition(s, activity_threshold, world, 0.0, 1.0)
-    dw, sw = partition_weights(L, hbm_gbs, fp64_tflops)
-    return plan_partition(s, activity_threshold, world, dw, sw)
+        b = plan_partition(s, activity_threshold, world, 0.0, 1.0)
+    else:
+        dw, sw = partition_weights(L, hbm_gbs, fp64_tflops)
+        b = plan_partition(s, activity_threshold, world, dw, sw)
+    return align_bounds(b, ALIGN)
+
+
+ALIGN = 32
+
+
+def align_bounds(b, align: int = ALIGN) -> np.ndarray:
+    """Rounds the interior offsets of a partition to the nearest multiple of
+    `align` (ends kept), preserving monotonicity."""
+    b = np.asarray(b, dtype=np.int64).copy()
+    n = int(b[-1])
+    for i in range(1, len(b) - 1):
+        b[i] = min(n, max(int(b[i - 1]), int(np.rint(b[i] / align)) * align))
+    return b
 
 
 def max_over_ranks(value: float, dist=None, device=None) -> float:
