@@ -162,6 +162,14 @@ struct cvg_context {
   bool fused = false;      // CVG_FUSED: shallow tiles inside the deep kernel (L <= 32)
   int shallow_minb = 8;    // CVG_SHALLOW_MINB: shallow blocks per SM the register budget targets (8, 12, 16)
   bool strict = false;     // CVG_STRICT: reference rounding in every Newton update (all variants)
+  // CVG_CARVEOUT: shared-memory carveout (% of the 228 KB maximum) preferred
+  // by the deep and the shallow kernel.  One value for both: an SM runs the
+  // two concurrently only in a configuration that suits both, and 72 % (164
+  // KB shared: the deep block's ~127 KB + four 8 KB shallow blocks; 92 KB
+  // L1 left for the shallow kernel's row re-reads) measured 0.51 ms per f02
+  // step against 0.55 ms at 100 % (deep) / no preference (shallow), and
+  // without the occasional serialised schedule (0.70 ms) of mixed settings.
+  int carveout = 72;
   bool far32 = true;       // CVG_FAR32: FP32 far phase of the relaxed Newton solve
   long long chunk_cols = kChunkCols;  // CVG_CHUNK_COLS: host-call pipeline chunk
   int slots = 3;                      // CVG_SLOTS: workspaces used by host-buffer calls (1..kSlots)
@@ -176,6 +184,14 @@ struct cvg_context {
   int last_maxit = 100;
   long long last_n = 0;
   bool pending = false;
+  // CUDA graphs of device-resident calls (CVG_GRAPH=0: plain launches),
+  // keyed by the call's argument bytes and the workspace list buffer
+  struct GraphEntry {
+    std::vector<unsigned char> key;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = true;
 };
 
 namespace {
@@ -230,8 +246,7 @@ void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st,
                       (size_t)NW * cvg::deep_warp_doubles(NARROW, a.L) * sizeof(double);
   auto kern = cvg::deep_kernel<VAR, NARROW, NW, FUSED, SH, RELAX_SH>;
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // full shared-memory carveout, so shallow blocks still fit beside it
-  CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
   kern<<<ctx->num_sms, threads, smem, st>>>(a, b);
   CVG_CUDA(cudaGetLastError());
 }
@@ -287,17 +302,23 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   } else {
     const unsigned blocks = (unsigned)((b.n + cvg::kShallowThreads - 1) / cvg::kShallowThreads);
     const bool relax = VAR != cvg::kVarApprox && !strict;
+    void (*k)(cvg::ShallowArgs) = nullptr;
     if (sh && relax) {
-      if (dp && ctx->shallow_minb == 12) cvg::shallow_kernel<VAR, true, true, true, 12><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
-      else if (dp && ctx->shallow_minb == 16) cvg::shallow_kernel<VAR, true, true, true, 16><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
-      else if (dp) cvg::shallow_kernel<VAR, true, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
-      else cvg::shallow_kernel<VAR, true, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+      if (dp && ctx->shallow_minb == 12) k = cvg::shallow_kernel<VAR, true, true, true, 12>;
+      else if (dp && ctx->shallow_minb == 16) k = cvg::shallow_kernel<VAR, true, true, true, 16>;
+      else if (dp) k = cvg::shallow_kernel<VAR, true, true, true>;
+      else k = cvg::shallow_kernel<VAR, true, false, true>;
     } else if (sh && dp) {
-      cvg::shallow_kernel<VAR, true, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+      k = cvg::shallow_kernel<VAR, true, true>;
     } else if (sh) {
-      cvg::shallow_kernel<VAR, true, false><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+      k = cvg::shallow_kernel<VAR, true, false>;
     } else if (dp) {
-      cvg::shallow_kernel<VAR, false, true><<<blocks, cvg::kShallowThreads, 0, st>>>(b);
+      k = cvg::shallow_kernel<VAR, false, true>;
+    }
+    if (k) {
+      // same carveout as the deep kernel (launch_deep_t)
+      CVG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
+      k<<<blocks, cvg::kShallowThreads, 0, st>>>(b);
     }
   }
   CVG_CUDA(cudaGetLastError());
@@ -493,6 +514,8 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     ctx->num_sms = prop.multiProcessorCount;
     if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
     if (const char* e = getenv("CVG_STRICT")) ctx->strict = atoi(e) != 0;
+    if (const char* e = getenv("CVG_GRAPH")) ctx->use_graphs = atoi(e) != 0;
+    if (const char* e = getenv("CVG_CARVEOUT")) ctx->carveout = atoi(e);
     if (const char* e = getenv("CVG_FAR32")) ctx->far32 = atoi(e) != 0;
     if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
     if (const char* e = getenv("CVG_FUSED")) ctx->fused = atoi(e) != 0;
@@ -535,9 +558,68 @@ void cvg_context_free(cvg_context* ctx) {
   for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->ev_h0, ctx->ev_h1})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
+  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
+
+}  // extern "C"
+
+namespace {
+
+// One device-resident call as a CUDA graph (memsets, trigger, deep and
+// shallow kernels with the fork/join): captured on first use of an argument
+// set, replayed after -- one launch instead of ~8 stream operations, and
+// the graph's dependency edges start each kernel with less front-end delay
+// (fixed per-step cost matters at the small per-GPU shares of a
+// multi-GPU partition).
+void launch_graph(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int mask, const cvg_outputs* deep,
+                  const cvg_outputs* sh, cudaStream_t st) {
+  Workspace& w = ctx->ws[0];
+  if (mask & CVG_DEEP) w.groups.ensure((size_t)((in->n_columns + cvg::kGroupCols - 1) / cvg::kGroupCols));
+  std::vector<unsigned char> key;
+  auto put = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    key.insert(key.end(), b, b + n);
+  };
+  const cvg_outputs none{};
+  put(in, sizeof(*in));
+  put(o, sizeof(*o));
+  put(&mask, sizeof(mask));
+  put((mask & CVG_DEEP) ? deep : &none, sizeof(none));
+  put((mask & CVG_SHALLOW) ? sh : &none, sizeof(none));
+  put(&w.groups.p, sizeof(w.groups.p));
+  put(&w.groups.cap, sizeof(w.groups.cap));
+  for (auto& g : ctx->graphs)
+    if (g.key == key) {
+      CVG_CUDA(cudaGraphLaunch(g.exec, st));
+      return;
+    }
+  cudaGraph_t graph = nullptr;
+  CVG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+  try {
+    enqueue(ctx, w, in, o, mask, deep, sh, st, nullptr);
+  } catch (...) {
+    cudaStreamEndCapture(st, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  CVG_CUDA(cudaStreamEndCapture(st, &graph));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CVG_CUDA(e);
+  if (ctx->graphs.size() >= 16) {
+    cudaGraphExecDestroy(ctx->graphs.front().exec);
+    ctx->graphs.erase(ctx->graphs.begin());
+  }
+  ctx->graphs.push_back({std::move(key), exec});
+  CVG_CUDA(cudaGraphLaunch(exec, st));
+}
+
+}  // namespace
+
+extern "C" {
 
 cvg_status cvg_convect_async(cvg_context* ctx, const cvg_columns* in, const cvg_options* opts, int mask,
                              const cvg_outputs* deep, const cvg_outputs* sh, void* stream) {
@@ -556,7 +638,11 @@ cvg_status cvg_convect_async(cvg_context* ctx, const cvg_columns* in, const cvg_
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     cudaEvent_t* pe = nullptr;
     if (ctx->prof_on && ctx->prof_n < ctx->prof_cap) pe = &ctx->prof_ev[4 * ctx->prof_n++];
-    enqueue(ctx, ctx->ws[0], in, opts, mask, deep, sh, st, pe);
+    if (pe || ctx->trace_path || !ctx->use_graphs || in->n_columns == 0) {
+      enqueue(ctx, ctx->ws[0], in, opts, mask, deep, sh, st, pe);
+    } else {
+      launch_graph(ctx, in, opts, mask, deep, sh, st);
+    }
     ctx->last_mask = mask;
     ctx->last_maxit = opts->newton_max_iter;
     ctx->last_n = in->n_columns;

@@ -21,24 +21,39 @@ from . import plan_partition
 MEAN_UPDATES = 694.0
 BYTES_PER_COLUMN_30 = 1482.0
 
+# Measured per-unit step times on one B200 at L = 30 (the analogue of the
+# reference's calibrate(), hetero.cpp:110-163): a least-squares fit of the
+# f02 step over its 1/2/4/8-way shares (bench.py --slice R/W) gives
+# t = 21 us + 1.21 ns per triggered column + 0.19 ns per column -- a
+# triggered column costs 6.3 plain columns, not the 4.0 of the FLOP/byte
+# model (the overlapped shallow kernel hides part of its bytes).
+MEASURED_NS_PER_TRIGGERED = 1.21
+MEASURED_NS_PER_COLUMN = 0.19
 
-def partition_weights(L: int = 30, hbm_gbs: float = 6558.7, fp64_tflops: float = 34.0):
-    deep_w = 159.0 * L + 37.0 * MEAN_UPDATES
-    bytes_per_col = 8 + 2 * 8 * L + 2 * (2 * 8 * L + 17)
-    shallow_w = bytes_per_col * (fp64_tflops * 1e12) / (hbm_gbs * 1e9)
-    return deep_w, shallow_w
+
+def partition_weights(L: int = 30, hbm_gbs: float = 6558.7, fp64_tflops: float = 34.0, mode: str = "balanced"):
+    """(deep_weight, shallow_weight) for cvg_plan_partition: measured B200
+    per-unit times ("balanced") or the FLOP/byte model ("model")."""
+    if mode == "model":
+        deep_w = 159.0 * L + 37.0 * MEAN_UPDATES
+        bytes_per_col = 8 + 2 * 8 * L + 2 * (2 * 8 * L + 17)
+        shallow_w = bytes_per_col * (fp64_tflops * 1e12) / (hbm_gbs * 1e9)
+        return deep_w, shallow_w
+    return MEASURED_NS_PER_TRIGGERED * L / 30.0, MEASURED_NS_PER_COLUMN * L / 30.0
 
 
 def rank_bounds(s, activity_threshold: float, world: int, mode: str = "balanced", L: int = 30,
                 hbm_gbs: float = 6558.7, fp64_tflops: float = 34.0) -> np.ndarray:
-    """world + 1 column offsets; rank r owns [b[r], b[r+1]).  Interior
-    boundaries are rounded to multiples of ALIGN columns (a rank's rows then
-    start on 256-byte boundaries and its 4-column groups are whole sectors;
-    the rounding moves at most 16 columns per boundary)."""
+    """world + 1 column offsets; rank r owns [b[r], b[r+1]).  mode:
+    "balanced" (measured per-unit costs), "model" (FLOP/byte model) or
+    "naive" (equal columns, StaticBlock).  Interior boundaries are rounded
+    to multiples of ALIGN columns (a rank's rows then start on 256-byte
+    boundaries and its 4-column groups are whole sectors; the rounding moves
+    at most 16 columns per boundary)."""
     if mode == "naive":
         b = plan_partition(s, activity_threshold, world, 0.0, 1.0)
     else:
-        dw, sw = partition_weights(L, hbm_gbs, fp64_tflops)
+        dw, sw = partition_weights(L, hbm_gbs, fp64_tflops, mode)
         b = plan_partition(s, activity_threshold, world, dw, sw)
     return align_bounds(b, ALIGN)
 
