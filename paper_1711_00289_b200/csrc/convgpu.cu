@@ -192,6 +192,7 @@ struct cvg_context {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
+  bool reset_kernel = true;   // CVG_RESET_KERNEL: one reset launch instead of three memsets
 };
 
 namespace {
@@ -337,9 +338,14 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
              const cvg_outputs* deep, const cvg_outputs* sh, cudaStream_t st, cudaEvent_t* pe) {
   const long long n = in->n_columns;
   const int L = in->n_levels;
-  CVG_CUDA(cudaMemsetAsync(w.counters.p, 0, 4 * sizeof(int), st));
-  CVG_CUDA(cudaMemsetAsync(w.cursor.p, 0, 17 * sizeof(unsigned long long), st));
-  CVG_CUDA(cudaMemsetAsync(w.err.p, 0xff, 2 * sizeof(unsigned long long), st));
+  if (ctx->reset_kernel) {
+    cvg::reset_call_words_kernel<<<1, 32, 0, st>>>(w.counters.p, 4, w.cursor.p, 17, w.err.p, 2);
+    CVG_CUDA(cudaGetLastError());
+  } else {
+    CVG_CUDA(cudaMemsetAsync(w.counters.p, 0, 4 * sizeof(int), st));
+    CVG_CUDA(cudaMemsetAsync(w.cursor.p, 0, 17 * sizeof(unsigned long long), st));
+    CVG_CUDA(cudaMemsetAsync(w.err.p, 0xff, 2 * sizeof(unsigned long long), st));
+  }
   if (n == 0) return;
   const bool do_deep = (mask & CVG_DEEP) != 0, do_sh = (mask & CVG_SHALLOW) != 0;
   const bool strict = ctx->strict || (o->flags & CVG_FLAG_STRICT) != 0;
@@ -515,6 +521,7 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
     if (const char* e = getenv("CVG_STRICT")) ctx->strict = atoi(e) != 0;
     if (const char* e = getenv("CVG_GRAPH")) ctx->use_graphs = atoi(e) != 0;
+    if (const char* e = getenv("CVG_RESET_KERNEL")) ctx->reset_kernel = atoi(e) != 0;
     if (const char* e = getenv("CVG_CARVEOUT")) ctx->carveout = atoi(e);
     if (const char* e = getenv("CVG_FAR32")) ctx->far32 = atoi(e) != 0;
     if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);

@@ -72,6 +72,16 @@ __device__ __forceinline__ double max0(double x) { return (0.0 < x) ? x : 0.0; }
 constexpr int kTrigThreads = 256;
 constexpr int kGroupCols = 4;
 
+// Per-call words of a workspace reset in one launch (instead of three
+// memsets): counts, cursors to 0, failure keys to "none".
+__global__ void reset_call_words_kernel(int* counts, int n_counts, unsigned long long* cursor, int n_cursor,
+                                        unsigned long long* err, int n_err) {
+  const int t = threadIdx.x;
+  if (t < n_counts) counts[t] = 0;
+  if (t < n_cursor) cursor[t] = 0;
+  if (t < n_err) err[t] = ~0ULL;
+}
+
 __global__ void __launch_bounds__(kTrigThreads)
 trigger_groups_kernel(const double* __restrict__ s, long long n, double thr, long long first_col,
                       long long* __restrict__ groups, int* __restrict__ counts,
