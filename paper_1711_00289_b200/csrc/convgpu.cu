@@ -144,6 +144,27 @@ constexpr long long kChunkCols = 262144;     // columns per host-buffer pipeline
 
 }  // namespace
 
+namespace {
+// Device state of one leg: T, q [L][n] (ld = n) and the selected kernel's
+// outputs.
+struct LegBufs {
+  DevBuf<double> T, q;
+};
+
+struct LoopBufs {
+  DevBuf<double> s, oT, oq, op;
+  DevBuf<long long> ow;
+  DevBuf<uint8_t> ox;
+  cvg_outputs outs(long long n) {
+    return cvg_outputs{oT.p, oq.p, op.p, ow.p, ox.p, n, 1};
+  }
+  void ensure(long long n, int L) {
+    s.ensure(n); oT.ensure((size_t)n * L); oq.ensure((size_t)n * L); op.ensure(n); ow.ensure(n); ox.ensure(n);
+  }
+};
+
+}  // namespace
+
 struct cvg_context {
   int device = 0;
   int num_sms = 0;
@@ -192,6 +213,12 @@ struct cvg_context {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
+  // cvg_timestep state, kept across calls (the reference's persistent
+  // buffers, hetero.hpp:44)
+  LoopBufs loop;
+  LegBufs leg;
+  DevBuf<unsigned long long> loop_err;
+  DevBuf<unsigned> loop_flag;
   bool reset_kernel = true;   // CVG_RESET_KERNEL: one reset launch instead of three memsets
 };
 
@@ -566,6 +593,8 @@ void cvg_context_free(cvg_context* ctx) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  for (auto* b : {&ctx->loop.s, &ctx->loop.oT, &ctx->loop.oq, &ctx->loop.op, &ctx->leg.T, &ctx->leg.q}) b->release();
+  ctx->loop.ow.release(); ctx->loop.ox.release(); ctx->loop_err.release(); ctx->loop_flag.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -967,24 +996,6 @@ void cvg_host_free(void* p) {
 
 namespace {
 
-// Device state of one leg: T, q [L][n] (ld = n) and the selected kernel's
-// outputs.
-struct LegBufs {
-  DevBuf<double> T, q;
-};
-
-struct LoopBufs {
-  DevBuf<double> s, oT, oq, op;
-  DevBuf<long long> ow;
-  DevBuf<uint8_t> ox;
-  cvg_outputs outs(long long n) {
-    return cvg_outputs{oT.p, oq.p, op.p, ow.p, ox.p, n, 1};
-  }
-  void ensure(long long n, int L) {
-    s.ensure(n); oT.ensure((size_t)n * L); oq.ensure((size_t)n * L); op.ensure(n); ow.ensure(n); ox.ensure(n);
-  }
-};
-
 unsigned elem_blocks(long long n, int L) { return (unsigned)((n * L + 255) / 256); }
 
 // One step of `kernel` over a device leg, its failure words copied to
@@ -1032,17 +1043,10 @@ cvg_status cvg_timestep(cvg_context* ctx, long long n, int L, long long ld, cons
     if (stats) std::memset(stats, 0, sizeof(*stats));
     if (stats) stats->failing_column = -1;
     cudaStream_t st = ctx->stream;
-    LoopBufs lb;
-    LegBufs leg;
-    DevBuf<unsigned long long> err;
-    DevBuf<unsigned> flag;
-    struct Free {
-      LoopBufs& lb; LegBufs& leg; DevBuf<unsigned long long>& err; DevBuf<unsigned>& flag;
-      ~Free() {
-        for (auto* b : {&lb.s, &lb.oT, &lb.oq, &lb.op, &leg.T, &leg.q}) b->release();
-        lb.ow.release(); lb.ox.release(); err.release(); flag.release();
-      }
-    } guard{lb, leg, err, flag};
+    LoopBufs& lb = ctx->loop;
+    LegBufs& leg = ctx->leg;
+    DevBuf<unsigned long long>& err = ctx->loop_err;
+    DevBuf<unsigned>& flag = ctx->loop_flag;
     lb.ensure(std::max(n, 1LL), L);
     leg.T.ensure((size_t)std::max(n, 1LL) * L);
     leg.q.ensure((size_t)std::max(n, 1LL) * L);
