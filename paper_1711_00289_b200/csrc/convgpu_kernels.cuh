@@ -988,11 +988,15 @@ __global__ void __launch_bounds__(kShTile, 1) shallow_tma_kernel(ShallowArgs a) 
 constexpr int kDeepWarps = 20;
 constexpr int kDeepWarpsOverlap = 12;
 
-// Register cap per thread: the register file divided over one block of NW
-// warps (the kernel needs ~94, so 12 and 16 warps are unconstrained).
+// Register cap per thread.  Blocks of up to 16 warps run beside the
+// shallow kernel (overlap mode): they get the register file minus three
+// shallow blocks (3 x 128 threads x 64 registers), so three shallow blocks
+// always fit (at 12 warps the uncapped kernel took 107 -> 112 registers and
+// left room for two); larger blocks run alone and get the whole file.
 template <int NW>
 constexpr int deep_max_regs() {
-  return ((65536 / (NW * 32)) & ~7) > 255 ? 255 : ((65536 / (NW * 32)) & ~7);
+  constexpr int budget = NW <= 16 ? 65536 - 3 * 128 * 64 : 65536;
+  return ((budget / (NW * 32)) & ~7) > 255 ? 255 : ((budget / (NW * 32)) & ~7);
 }
 
 // FUSED: also runs the shallow scheme (SH) or only the deep zero-fill (!SH)
