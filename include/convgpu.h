@@ -82,7 +82,7 @@ typedef struct cvg_options {
  * it only by rounding noise inside the parity window). */
 #define CVG_FLAG_STRICT 1
 /* cvg_options.flags: no FP32 far phase in the relaxed Newton solve (the far
- * steps of Exact/StrengthReduced run in FP32 until |resid| <= 0.25, then the
+ * steps of Exact/StrengthReduced run in FP32 until |resid| <= 0.1, then the
  * solve continues in FP64). */
 #define CVG_FLAG_NO_FAR32 2
 
