@@ -88,3 +88,17 @@ def test_partition_rejects_bad_arguments():
     lib = P.load_library()
     assert lib.cvg_plan_partition(-1, None, 0.5, 2, 0.0, 1.0, b.ctypes.data) == 1
     assert lib.cvg_plan_partition(5, None, 0.5, 0, 0.0, 1.0, b.ctypes.data) == 1
+
+
+def test_partition_bounds_are_aligned_and_monotone():
+    from paper_1711_00289_b200 import gridgen, multigpu
+    s, _, _ = gridgen.make_config("c5_50", shape=(48, 64), seed=4)
+    for world in (1, 2, 3, 8):
+        for mode in ("balanced", "model", "naive"):
+            b = multigpu.rank_bounds(s, 0.5, world, mode)
+            assert b[0] == 0 and b[-1] == s.size and len(b) == world + 1
+            assert np.all(np.diff(b) >= 0)
+            assert np.all(b[1:-1] % multigpu.ALIGN == 0)
+    # rounding moves a boundary by at most ALIGN / 2
+    raw = P.plan_partition(s, 0.5, 8, *multigpu.partition_weights())
+    assert np.max(np.abs(multigpu.align_bounds(raw) - raw)) <= multigpu.ALIGN // 2

@@ -286,3 +286,51 @@ def test_staging_bytes_follow_reference_pack(ctx, kernels, nk):
     st = ctx.last_stats
     bi, bo = O.ref_packed_bytes(s.size, T.shape[0], send_scalars=False)
     assert st.h2d_bytes == bi and st.d2h_bytes == nk * bo
+
+
+def test_graph_replay_tracks_buffer_contents(ctx):
+    """Device-resident calls replay a captured CUDA graph per argument set:
+    new input VALUES in the same buffers, a second output set (new graph)
+    and a latched failure after replay all behave like fresh launches."""
+    import torch
+    dev = torch.device("cuda", 0)
+    s0, T0, q0 = G.make_config("c1", n=3000, seed=21)
+    L, n = T0.shape
+    ds, dT, dq = (torch.from_numpy(a).to(dev) for a in (s0, T0, q0))
+
+    def outs():
+        return (torch.empty((L, n), dtype=torch.float64, device=dev), torch.empty((L, n), dtype=torch.float64, device=dev),
+                torch.empty(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.int64, device=dev),
+                torch.empty(n, dtype=torch.uint8, device=dev))
+    sets = [(outs(), outs()), (outs(), outs())]
+    for it, seed in enumerate((21, 22, 23, 24)):
+        s, T, q = G.make_config("c1", n=3000, seed=seed)
+        ds.copy_(torch.from_numpy(s)); dT.copy_(torch.from_numpy(T)); dq.copy_(torch.from_numpy(q))
+        do, so = sets[it % 2]
+        for _ in range(2):
+            ctx.convect_async(ds, dT, dq, do, so)
+        st = ctx.check()
+        assert st.n_triggered == int((s > 0.5).sum())
+        both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in do]), O.convection("deep", s, T, q))
+        both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in so]), O.convection("shallow", s, T, q))
+    ds[11] = float("nan")
+    ctx.convect_async(ds, dT, dq, *sets[0])
+    with pytest.raises(P.KernelError) as e:
+        ctx.check()
+    assert e.value.column == 11
+    ds[11] = 0.3
+    ctx.convect_async(ds, dT, dq, *sets[0])
+    ctx.check()   # the failure word was reset for the next call
+
+
+def test_option_flags(ctx):
+    s, T, q = G.make_config("c1", n=256, seed=2)
+    o = P.KernelOptions()
+    o.flags = 4   # unknown bit
+    with pytest.raises(ValueError):
+        ctx.convect(s, T, q, o)
+    a, _ = ctx.convect(s, T, q, P.KernelOptions(far32=False))
+    b, _ = ctx.convect(s, T, q, P.KernelOptions(far32=False, strict=True))
+    od = O.convection("deep", s, T, q)
+    both_close(a, od)
+    both_close(b, od)
