@@ -36,10 +36,14 @@ enum : int { kVarExact = 0, kVarReduced = 1, kVarApprox = 2 };
 
 // Phase-clock instrumentation of the deep worker (debug builds with
 // -DCVG_PHASE_CLOCKS only): per-phase SM cycles summed over warps.
+// Accumulated per block in shared memory (flushed once per block at the
+// kernel's end): per-column global atomics on 8 addresses from every warp
+// slowed the instrumented kernel 2.6x and distorted the split.
 #ifdef CVG_PHASE_CLOCKS
 __device__ unsigned long long g_phase[8];
+__shared__ unsigned long long s_phase[8];
 #define CVG_PCLK(v) const long long v = clock64()
-#define CVG_PACC(i, a, b) if (lane == 0) atomicAdd(&g_phase[i], (unsigned long long)((b) - (a)))
+#define CVG_PACC(i, a, b) if (lane == 0) atomicAdd(&s_phase[i], (unsigned long long)((b) - (a)))
 #else
 #define CVG_PCLK(v)
 #define CVG_PACC(i, a, b)
@@ -252,6 +256,7 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
     const double tol = a.tol;
     int left = maxit + 1;   // updates still allowed (the loop may take one
                             // more than maxit; newton_finish then fails it)
+    CVG_PCLK(pf0);
     {
       float fte = (float)guess, ftp = fte, fee = (float)e0, fep = fee;
       float fhe = (float)he, fhp = (float)hp;
@@ -263,6 +268,11 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
       }
       te = fte;
       tp = ftp;
+    }
+    {
+      CVG_PCLK(pf1);
+      const int lane = threadIdx.x & 31;
+      CVG_PACC(5, pf0, pf1);   // FP32 far loop
     }
     ee = exp_relaxed1(kRC, te, tab1_addr);
     ep = exp_relaxed1(kRC, tp, tab1_addr);
@@ -387,6 +397,10 @@ __device__ __forceinline__ bool deep_level(const DeepArgs& a, const double2* s_t
 // columns, lane i sums column i's terms in k order (physics.cpp:161) -- one
 // warp instruction serves kBatch columns instead of one.
 constexpr int kDeepChunk = 1;   // list entries (groups) claimed per atomic (power of 2)
+#ifndef CVG_STAGE_REGS
+#define CVG_STAGE_REGS 1
+#endif
+constexpr bool kStageRegs = CVG_STAGE_REGS;   // next column prefetched into registers (else cp.async)
 
 // Issued by lane 0 only, at cursor + lane (= cursor): an address ptxas
 // cannot prove warp-uniform, so it does not rewrite the atomic into its
@@ -486,13 +500,26 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     }
     cp_async_commit();
   };
+  // kStageRegs: the next column's (s, T[lane], q[lane]) are prefetched into
+  // registers with read-only loads instead of cp.async into shared memory
+  double nx_s = 0.0, nx_T = 0.0, nx_q = 0.0;
+  auto prefetch = [&](long long cc) {
+    nx_s = __ldg(a.s + cc);
+    if (lane < L) {
+      nx_T = __ldg(T_row + cc);
+      nx_q = __ldg(q_row + cc);
+    }
+  };
   if (e >= 0) {
   long long g = e >> 4;
   unsigned m = (unsigned)(e & 15), rem = m;
   int i = __ffs(rem) - 1;
   rem &= rem - 1;
   long long c = g * kGroupCols + i;
-  if (NARROW) stage(c, 0);
+  if (NARROW) {
+    if (kStageRegs) prefetch(c);
+    else stage(c, 0);
+  }
   for (;;) {
     CVG_PCLK(ph0);
     // the column after this one: the group's next, or the next group's first
@@ -500,7 +527,20 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     if (rem) cn = g * kGroupCols + (__ffs(rem) - 1);
     else if (en >= 0) cn = (en >> 4) * kGroupCols + (__ffs((unsigned)(en & 15)) - 1);
     double sc, T_c = 0.0, q_c = 0.0;
-    if (NARROW) {
+    if (NARROW && kStageRegs) {
+      sc = nx_s;
+      T_c = nx_T;
+      q_c = nx_q;
+#ifdef CVG_PHASE_CLOCKS
+      {
+        double chk = sc + T_c + q_c;   // force the staged values here
+        asm volatile("" : "+d"(chk));
+        CVG_PCLK(phw);
+        CVG_PACC(6, ph0, phw);   // wait for the staged column
+      }
+#endif
+      if (cn >= 0) prefetch(cn);
+    } else if (NARROW) {
       cp_async_wait_all();
       const unsigned d = st_addr + buf * 768;
       sc = lds_f64(d);
@@ -508,6 +548,14 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
         T_c = lds_f64(d + 256);
         q_c = lds_f64(d + 512);
       }
+#ifdef CVG_PHASE_CLOCKS
+      {
+        double chk = sc + T_c + q_c;   // force the staged values here
+        asm volatile("" : "+d"(chk));
+        CVG_PCLK(phw);
+        CVG_PACC(6, ph0, phw);   // wait for the staged column
+      }
+#endif
       if (cn >= 0) stage(cn, buf ^ 1);
       buf ^= 1;
     } else {
@@ -1004,6 +1052,9 @@ constexpr int deep_max_regs() {
 template <int VAR, bool NARROW, int NW, bool FUSED = false, bool SH = true, bool RELAX_SH = false>
 __global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a, ShallowArgs b) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+#ifdef CVG_PHASE_CLOCKS
+  if (threadIdx.x < 8) s_phase[threadIdx.x] = 0;
+#endif
   if (a.trace && threadIdx.x == 0) {
     a.trace[3 * blockIdx.x] = smid();
     a.trace[3 * blockIdx.x + 1] = gtimer();
@@ -1043,6 +1094,10 @@ __global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a, Shallow
   } else {
     deep_worker<VAR, NARROW>(a, s_tab, tab1_addr, s_warp, s_gwork[wib], s_gok[wib], s_gpr[wib], lane);
   }
+#ifdef CVG_PHASE_CLOCKS
+  __syncthreads();
+  if (threadIdx.x < 8) atomicAdd(&g_phase[threadIdx.x], s_phase[threadIdx.x]);
+#endif
   if (a.trace) {
     __syncthreads();
     if (threadIdx.x == 0) a.trace[3 * blockIdx.x + 2] = gtimer();

@@ -5,7 +5,7 @@ import ctypes as C
 import os
 import sys
 
-os.environ["CONVGPU_LIB"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libconvgpu_phases.so")
+os.environ["CONVGPU_LIB"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("PHASES_LIB", "libconvgpu_phases.so"))
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -30,7 +30,7 @@ for rep in range(3):
     ctx.check(st)
     P.load_library().cvg_debug_phases(out)
 names = ["prologue (wait, stage, guess, e0)", "levels (m, y, Newton, sin, tend)", "reductions",
-         "group flush + advance", "  of which relaxed Newton loop"]
+         "group flush + advance", "  of which relaxed FP64 Newton loop", "  of which FP32 far loop", "  of which staged-column wait"]
 tot = sum(out[i] for i in range(4))
 trig = int((s > 0.5).sum())
 for i, nm in enumerate(names):
