@@ -23,12 +23,15 @@ BYTES_PER_COLUMN_30 = 1482.0
 
 # Measured per-unit step times on one B200 at L = 30 (the analogue of the
 # reference's calibrate(), hetero.cpp:110-163): a least-squares fit of the
-# f02 step over its 1/4/8-way shares (bench.py --slice R/W, two rounds of
-# refit) gives t = 22 us + 1.34 ns per triggered column + 0.155 ns per
-# column -- a triggered column costs ~8.6 plain columns, not the 4.0 of the
-# FLOP/byte model (the overlapped shallow kernel hides part of its bytes).
-MEASURED_NS_PER_TRIGGERED = 1.34
-MEASURED_NS_PER_COLUMN = 0.155
+# f02 step over its 1/4/8-way shares (bench.py --slice R/W) gives
+# t = 22 us + 1.34 ns per triggered column + 0.155 ns per column; a further
+# hand refit of the ratio on the per-rank times (deep-heavy shares run
+# their tail with the shallow kernel gone and only the overlap-size deep
+# blocks, so they cost more than linear) settles at 11: a triggered column
+# weighs 11 plain columns (the FLOP/byte model says 4.0), giving per-rank
+# times within 6 % of each other at 8 ranks and 7 % at 4.
+MEASURED_NS_PER_TRIGGERED = 1.45
+MEASURED_NS_PER_COLUMN = 0.132
 
 
 def partition_weights(L: int = 30, hbm_gbs: float = 6558.7, fp64_tflops: float = 34.0, mode: str = "balanced"):
