@@ -476,7 +476,32 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
   long long jn = advance(j);
   long long e = entry(j), en = entry(jn);
   long long jnn = jn < G ? advance(jn) : G;
-  long long enn = entry(jnn);
+  // kStageRegs: the entry after next arrives by cp.async into one of two
+  // per-warp shared slots (the staging area is free then), so no register
+  // waits for it -- a plain load's result had to be copied into the
+  // rotating entry registers right away, and that copy stalled on the load
+  // (5 % of the kernel's warp samples)
+  const unsigned ent_addr = smem_u32(s_warp);
+  int eslot = 0;
+  auto fetch_entry = [&](long long x) {
+    if (lane == 0) {
+      const unsigned d = ent_addr + 8 * eslot;
+      if (x < G) cp_async8_u32(d, a.groups + x);
+      else asm volatile("st.shared.s64 [%0], %1;" ::"r"(d), "l"(-1LL) : "memory");
+      cp_async_commit();
+    }
+  };
+  auto take_entry = [&]() -> long long {
+    if (lane == 0) cp_async_wait_all();
+    __syncwarp();
+    long long v;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(ent_addr + 8 * eslot) : "memory");
+    eslot ^= 1;
+    return v;
+  };
+  long long enn = 0;
+  if (NARROW && kStageRegs) fetch_entry(jnn);
+  else enn = entry(jnn);
   int groups_done = 0;
   double* s_outT = s_warp + 2 * 3 * 32;   // NARROW: [4][32]
   double* s_outQ = s_outT + kGroupCols * 32;
@@ -571,7 +596,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     const long long col = a.first_col + c;
     int wl = 0;
     bool ok_all = true;
-    double term_l = 0.0;   // tree_precip: this lane's precipitation term
+    double term_l = 0.0;
     // NARROW (L <= 32): one level per lane, its (T, q) staged; wide columns
     // loop over levels lane, lane + 32, ... with plain loads
     for (int k = lane; k < L; k += 32) {
@@ -603,8 +628,6 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     const int wsum = __reduce_add_sync(0xffffffffu, wl);
     const bool ok = __all_sync(0xffffffffu, ok_all);
     if (NARROW && a.tree_precip) {
-      // relaxed path: precip as a fixed-shape warp tree (terms >= 0, so
-      // within 30 ulp of the reference's k-order sum, physics.cpp:161)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) term_l = add(term_l, __shfl_xor_sync(0xffffffffu, term_l, o));
       if (lane == 0) s_gpr[i] = term_l;
@@ -688,11 +711,12 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       if (en < 0) break;
       // next group; load the entry after it
       e = en;
-      en = enn;
+      en = (NARROW && kStageRegs) ? take_entry() : enn;
       j = jn;
       jn = jnn;
       jnn = jn < G ? advance(jn) : G;
-      enn = entry(jnn);
+      if (NARROW && kStageRegs) fetch_entry(jnn);
+      else enn = entry(jnn);
       g = e >> 4;
       m = (unsigned)(e & 15);
       rem = m;
