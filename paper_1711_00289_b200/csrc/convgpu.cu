@@ -252,10 +252,13 @@ bool valid_options(const cvg_options* o, std::string* why) {
 // high-word bound lim of the targets y in [0.25, 16) for which the FP32 far
 // phase and the relaxed update are both admissible -- relaxed_ok(y, tol)
 // holds iff the exponent of y is <= that of tol + 40 (y >= 1) or tol >=
-// 2^-40 (y < 1), and the far phase needs tol <= 1e-6.  Empty window (lim =
+// 2^-40 (y < 1), and the far phase needs tol <= 1e-9 (so that at least three
+// FP64 steps follow the switch and contract the FP32 iterate's error below
+// rounding noise; tests/test_parity_gpu.py test_hot_path_window_edges saw
+// 1e-12-sized tendency differences at tol 1e-6).  Empty window (lim =
 // hi(0.25)) when the far phase is off.
 static int far_window_limit(double tol, bool enabled) {
-  if (!enabled || !(tol <= 1e-6) || !(tol >= 0x1.0p-40)) return cvg::kFarWindowLo;
+  if (!enabled || !(tol <= 1e-9) || !(tol >= 0x1.0p-40)) return cvg::kFarWindowLo;
   unsigned long long bits;
   memcpy(&bits, &tol, sizeof bits);
   const int tol_exp = (int)(bits >> 32) & 0x7ff00000;

@@ -591,7 +591,8 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     const double rho = add(1.0, mul(kMC.c005, sc));
     const double e0 = deep_exp<VAR>(mul(kMC.c005, guess), s_tab);
     const double c0 = add(e0, mul(kMC.c001, guess));
-    const bool col_far = guess < 1190.0;   // far phase: exp(0.05 guess) < 2^86
+    // far phase: guesses below 512 (FP32 ulp of t <= 6e-5, <= ~25 far steps)
+    const bool col_far = guess < 512.0;
     CVG_PCLK(ph1);
     const long long col = a.first_col + c;
     int wl = 0;

@@ -236,3 +236,24 @@ def test_far32_against_fp64_update(ctx, cfg, kw, variant):
     check(b, od, "deep")
     check(a, {"tend_T": b.tend_T, "tend_q": b.tend_q, "precip": b.precip, "work": b.work_units,
               "exited": b.exited_early}, "deep", margin=od.margin)
+
+
+@pytest.mark.parametrize("tol", [1e-12, 1e-6, 2e-6, 2.0 ** -40, 1e-13])
+def test_hot_path_window_edges(ctx, tol):
+    """Targets y on both sides of the FP32/relaxed hot-path window [0.25, 16)
+    (colmath.cuh in_far_window), guesses on both sides of 1190 (s up to 7.4),
+    and tolerances at the window's limits (1e-6, 2^-40) and just outside:
+    every column, every path, against the oracle."""
+    Ts = np.concatenate([np.linspace(-2000.0, 16500.0, 61), [-750.0, -749.9, 15000.0, 15001.0]])
+    cols = [(s_, q_, T_) for s_ in (0.55, 0.9, 3.0, 7.38, 7.45) for q_ in (0.0, 0.02) for T_ in Ts]
+    n, L = len(cols), 30
+    s = np.array([c[0] for c in cols])
+    T = np.empty((L, n))
+    q = np.empty((L, n))
+    for j, (_, q_, T_) in enumerate(cols):
+        T[:, j] = T_ + np.linspace(0.0, 3.0, L)   # levels spread around the column's target
+        q[:, j] = q_
+    o = P.KernelOptions(newton_tol=tol)
+    deep, _ = ctx.convect(s, T, q, o, kernels=P.DEEP)
+    od = O.convection("deep", s, T, q, O.Options(newton_tol=tol))
+    check(deep, od, "deep")
