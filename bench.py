@@ -469,7 +469,8 @@ def run_gpu_arm(args):
         "kernels_ms": {"trigger_groups": trig_ms, "deep": deep_ms, "shallow_tail_after_deep": sh_ms,
                        "schedule": "trigger/group compaction -> deep (main stream) || shallow + zero-fill of "
                                    "untriggered groups (side stream, concurrent)"},
-        "gpu_launches": 3 * K,
+        # per step: reset of the per-call words, trigger/compaction, deep, shallow + zero-fill
+        "gpu_launches": 4 * K,
         "e2e": e2e,
         "feedback_loop": loop,
         "cpu_baseline": cpu,
