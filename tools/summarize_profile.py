@@ -45,12 +45,22 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "sm__cycles_active.avg", "sm__cycles_elapsed.avg"]
 caps = []
+OPS = ["smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed",
+       "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed",
+       "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed"]
 for r in R[2:]:
     d = {"kernel": r[H.index("Kernel Name")].split("(")[0].replace("void ", "").strip()}
     for w in want:
         if w in H:
             d[w] = r[H.index(w)] + (" " + U[H.index(w)] if U[H.index(w)] else "")
+    # ncu-measured FP64 work (SURVEY 8d cross-check): 2 DFMA + DADD + DMUL
+    # thread-ops, from the per-cycle rates times the elapsed cycles
+    if all(o in H for o in OPS) and "sm__cycles_elapsed.avg" in H:
+        cyc = float(r[H.index("sm__cycles_elapsed.avg")].replace(",", ""))
+        fma, dadd, dmul = (float(r[H.index(o)].replace(",", "")) * cyc for o in OPS)
+        d["fp64 flops (2 dfma + dadd + dmul, ncu)"] = f"{2 * fma + dadd + dmul:.4g}"
     caps.append(d)
+want.append("fp64 flops (2 dfma + dadd + dmul, ncu)")
 
 lines = [f"# {tag} ncu summary (config {config}, bench.py --steps 3 --warmup 3)", "",
          "## Launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)", "",
