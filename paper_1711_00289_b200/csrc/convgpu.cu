@@ -213,6 +213,7 @@ struct cvg_context {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
+  int deep_tpc = 2;           // CVG_DEEP_TPC: thread-per-column deep kernel: 0 never, 1 always, 2 for large calls
   // cvg_timestep state, kept across calls (the reference's persistent
   // buffers, hetero.hpp:44)
   LoopBufs loop;
@@ -303,7 +304,25 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   const bool ov = ctx->overlap && dp;
   const cudaStream_t main = st;
   if (ov) CVG_CUDA(cudaEventRecord(w.ev_fork, st));
-  if (dp) {
+  // Thread-per-column deep kernel for large calls (the f02 grid on one or
+  // two GPUs): 0.445 vs 0.508 ms per f02 step, 0.234 vs 0.251 ms on a 2-way
+  // share; its 32-column claims take ~90 us per warp, so from 4-way shares
+  // down the warp-per-column kernel's finer claims win (0.138 vs 0.152 ms,
+  // 0.078 vs 0.089 ms at 8-way).  CVG_DEEP_TPC: 0 never, 1 always, 2 auto.
+  const bool tpc = dp && a.L <= 32 &&
+                   (ctx->deep_tpc == 1 || (ctx->deep_tpc == 2 && a.n >= cvg::kTpcMinColumns));
+  if (tpc) {
+    const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
+                        (size_t)cvg::kExpTableSize * cvg::kTab1Copies * sizeof(double);
+    // beside the shallow kernel: one 12-warp block per SM (registers capped
+    // so three shallow blocks fit); alone: two 10-warp blocks per SM
+    auto kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
+    const int nwt = ov ? 12 : 10, blocks = ov ? 1 : 2;
+    CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
+    kern<<<ctx->num_sms * blocks, nwt * 32, smem, st>>>(a);
+    CVG_CUDA(cudaGetLastError());
+  } else if (dp) {
     // deep block size: kDeepWarpsOverlap leaves each SM room for three
     // shallow blocks beside the deep block; kDeepWarps when deep runs alone
     const int nw = ctx->deep_warps > 0 ? ctx->deep_warps : (ov ? cvg::kDeepWarpsOverlap : cvg::kDeepWarps);
@@ -551,6 +570,7 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_OVERLAP")) ctx->overlap = atoi(e) != 0;
     if (const char* e = getenv("CVG_STRICT")) ctx->strict = atoi(e) != 0;
     if (const char* e = getenv("CVG_GRAPH")) ctx->use_graphs = atoi(e) != 0;
+    if (const char* e = getenv("CVG_DEEP_TPC")) ctx->deep_tpc = atoi(e);
     if (const char* e = getenv("CVG_RESET_KERNEL")) ctx->reset_kernel = atoi(e) != 0;
     if (const char* e = getenv("CVG_CARVEOUT")) ctx->carveout = atoi(e);
     if (const char* e = getenv("CVG_FAR32")) ctx->far32 = atoi(e) != 0;

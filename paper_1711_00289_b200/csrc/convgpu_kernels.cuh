@@ -1130,6 +1130,93 @@ __global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a, Shallow
 }
 
 // ---------------------------------------------------------------------------
+// Thread-per-column deep kernel (large calls; CVG_DEEP_TPC):
+// a warp claims 8 listed groups (32 column slots, lane = slot), every lane
+// with a triggered column runs its column's levels in a loop (deep_level),
+// storing each level row as it goes (coalesced across the warp's lanes when
+// the groups are contiguous) and summing precip in k order (the
+// reference's order); lanes of untriggered slots write the zeros.
+// Calls with at least this many columns use it (convgpu.cu launch_kernels).
+constexpr long long kTpcMinColumns = 320000;
+
+template <int VAR, int NW, int REGCAP>
+__global__ void __maxnreg__(REGCAP) deep_tpc_kernel(DeepArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
+  double* s_tab1_all = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies);
+  if (VAR != kVarApprox) {
+    for (int i = threadIdx.x; i < kExpTableSize * kTabCopies; i += blockDim.x)
+      s_tab_all[i] = a.exp_tab[i / kTabCopies];
+    for (int i = threadIdx.x; i < kExpTableSize * kTab1Copies; i += blockDim.x)
+      s_tab1_all[i] = a.exp_tab[i / kTab1Copies].x;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const double2* s_tab = s_tab_all + (lane & (kTabCopies - 1));
+  const unsigned tab1_addr = opaque_u32(smem_u32(s_tab1_all + (lane & (kTab1Copies - 1))));
+  const long long G = *a.count;
+  const int L = a.L;
+  const unsigned lane_op = opaque_u32(lane);
+  for (;;) {
+    long long j = 0;
+    if (lane == 0) j = (long long)atomicAdd(a.cursor + lane_op, 8ULL);
+    j = __shfl_sync(0xffffffffu, j, 0);
+    if (j >= G) break;
+    const long long x = j + (lane >> 2);
+    const long long e = x < G ? a.groups[x] : -1;
+    const int slot = lane & 3;
+    const long long c = e >= 0 ? (e >> 4) * kGroupCols + slot : -1;
+    if (c < 0 || c >= a.n) continue;
+    const bool trig = (e >> slot) & 1;
+    double* pT = a.tend_T + c;
+    double* pQ = a.tend_q + c;
+    if (!trig) {
+      for (int k = 0; k < L; ++k) {
+        pT[(long long)k * a.ld_out] = 0.0;
+        pQ[(long long)k * a.ld_out] = 0.0;
+      }
+      a.precip[c] = 0.0;
+      a.work[c] = 0;
+      a.exited[c] = 1;
+      continue;
+    }
+    const double sc = a.s[c];
+    const double guess = add(24.0, mul(160.0, sc));
+    const double rho = add(1.0, mul(kMC.c005, sc));
+    const double e0 = deep_exp<VAR>(mul(kMC.c005, guess), s_tab);
+    const double c0 = add(e0, mul(kMC.c001, guess));
+    const bool col_far = guess < 512.0;
+    const double* Tr = a.T + c;
+    const double* qr = a.q + c;
+    double pr = 0.0;
+    long long wsum = 0;
+    bool ok = true;
+    double Tn = __ldg(Tr), qn = __ldg(qr);
+    for (int k = 0; k < L; ++k) {
+      const double T = Tn, q = qn;
+      if (k + 1 < L) {
+        Tn = __ldg(Tr + (long long)(k + 1) * a.ld_in);
+        qn = __ldg(qr + (long long)(k + 1) * a.ld_in);
+      }
+      double tT, tq, term;
+      int w;
+      if (!deep_level<VAR>(a, s_tab, tab1_addr, a.first_col + c, k, sc, rho, guess, e0, c0, col_far, T, q, tT,
+                           tq, term, w))
+        ok = false;
+      pT[(long long)k * a.ld_out] = tT;
+      pQ[(long long)k * a.ld_out] = tq;
+      pr = add(pr, term);   // physics.cpp:161, k order
+      wsum += w;
+    }
+    if (ok) {
+      a.precip[c] = pr;
+      a.work[c] = wsum;
+      a.exited[c] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Feedback loop (validate.cpp:113-206): perturb_lsb, advance, check_finite
 // and the RMS difference of two temperature fields.
 

@@ -258,3 +258,40 @@ def test_hot_path_window_edges(ctx, tol):
     deep, _ = ctx.convect(s, T, q, o, kernels=P.DEEP)
     od = O.convection("deep", s, T, q, O.Options(newton_tol=tol))
     check(deep, od, "deep")
+
+
+@pytest.fixture(scope="module")
+def tpc_ctx():
+    """The thread-per-column deep kernel forced on every call (CVG_DEEP_TPC=1;
+    by default only calls of >= 320k columns use it)."""
+    from conftest import env_context
+    c = env_context(CVG_DEEP_TPC="1")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("cfg,kw", CONFIGS, ids=[c for c, _ in CONFIGS])
+def test_thread_per_column_kernel_matches_oracle(tpc_ctx, cfg, kw, variant):
+    s, T, q = G.make_config(cfg, seed=17, **kw)
+    thr = G.config_threshold(cfg)
+    deep, sh = tpc_ctx.convect(s, T, q, P.KernelOptions(variant=variant, activity_threshold=thr))
+    oo = O.Options(variant=variant, activity_threshold=thr)
+    check(deep, O.convection("deep", s, T, q, oo), "deep", bitexact_work=(variant == 2))
+    check(sh, O.convection("shallow", s, T, q, oo), "shallow", bitexact_work=(variant == 2))
+
+
+@pytest.mark.parametrize("n", [1, 5, 31, 33, 1001])
+def test_thread_per_column_ragged_and_errors(tpc_ctx, n):
+    s, T, q = G.make_config("c1", n=n, seed=4)
+    deep, _ = tpc_ctx.convect(s, T, q)
+    check(deep, O.convection("deep", s, T, q), "deep")
+    if n >= 5:
+        s2 = s.copy()
+        s2[:] = 0.9
+        T2 = T.copy()
+        T2[7, n - 1] = np.nan
+        T2[3, n - 2] = np.nan
+        with pytest.raises(P.KernelError) as e:
+            tpc_ctx.deep_convection(s2, T2, q)
+        assert e.value.column == n - 2
