@@ -452,7 +452,9 @@ def run_gpu_arm(args):
                    "triggered_deep": int(n_trig), "partition": args.partition if ws > 1 else "single",
                    "l2": "inputs (425 MB) + outputs (880 MB) exceed the 126 MB L2; no flush needed",
                    "parallelism": f"column partition x{ws}, no collective"},
-        "roofline": {"bound": "fp64", "kernel": "deep_kernel", "achieved": achieved,
+        "roofline": {"bound": "fp64",
+                     "kernel": "deep_tpc_kernel" if n >= 320000 else "deep_kernel",
+                     "achieved": achieved,
                      "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                      "traffic": traffic,
                      "peak_source": "live DFMA probe on this GPU (cvg_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",

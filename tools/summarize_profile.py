@@ -78,7 +78,7 @@ for d in caps:
     lines.append("")
 open(os.path.join(prof, f"{tag}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
 
-deep = [d for d in caps if d["kernel"].startswith("cvg::deep_kernel") or "deep_kernel" in d["kernel"]]
+deep = [d for d in caps if "deep_kernel" in d["kernel"] or "deep_tpc_kernel" in d["kernel"]]
 if deep:
     d = deep[0]
     rd = float(d["dram__bytes_read.sum"].split()[0]); wr = float(d["dram__bytes_write.sum"].split()[0])
