@@ -1142,6 +1142,10 @@ constexpr long long kTpcMinColumns = 320000;
 template <int VAR, int NW, int REGCAP>
 __global__ void __maxnreg__(REGCAP) deep_tpc_kernel(DeepArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  if (a.trace && threadIdx.x == 0) {
+    a.trace[3 * blockIdx.x] = smid();
+    a.trace[3 * blockIdx.x + 1] = gtimer();
+  }
   double2* s_tab_all = reinterpret_cast<double2*>(smem_raw);
   double* s_tab1_all = reinterpret_cast<double*>(s_tab_all + kExpTableSize * kTabCopies);
   if (VAR != kVarApprox) {
@@ -1213,6 +1217,10 @@ __global__ void __maxnreg__(REGCAP) deep_tpc_kernel(DeepArgs a) {
       a.work[c] = wsum;
       a.exited[c] = 0;
     }
+  }
+  if (a.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.trace[3 * blockIdx.x + 2] = gtimer();
   }
 }
 
