@@ -397,10 +397,6 @@ __device__ __forceinline__ bool deep_level(const DeepArgs& a, const double2* s_t
 // columns, lane i sums column i's terms in k order (physics.cpp:161) -- one
 // warp instruction serves kBatch columns instead of one.
 constexpr int kDeepChunk = 1;   // list entries (groups) claimed per atomic (power of 2)
-#ifndef CVG_STAGE_REGS
-#define CVG_STAGE_REGS 1
-#endif
-constexpr bool kStageRegs = CVG_STAGE_REGS;   // next column prefetched into registers (else cp.async)
 
 // Issued by lane 0 only, at cursor + lane (= cursor): an address ptxas
 // cannot prove warp-uniform, so it does not rewrite the atomic into its
@@ -414,11 +410,11 @@ __device__ __forceinline__ long long claim_chunk(unsigned long long* cursor_plus
 
 // The group's per-column scalars live in s_gwork / s_gok / s_gpr [4].
 // Per-warp shared scratch of the deep worker, in doubles:
-//   NARROW: staging [2][3][32] (s, T[lane], q[lane] of the next column),
-//           group outputs tend_T, tend_q [4][32] each, precip terms [4][32]
+//   NARROW: [32] (two group-entry slots, padded), group outputs tend_T,
+//           tend_q [4][32] each, precip terms [4][32]
 //   wide:   precip terms [L] of the current column
 __host__ __device__ constexpr int deep_warp_doubles(bool narrow, int L) {
-  return narrow ? 2 * 3 * 32 + 3 * kGroupCols * 32 : L;
+  return narrow ? 32 + 3 * kGroupCols * 32 : L;
 }
 
 // The deep role of a warp: walks the group list until it is exhausted.
@@ -476,8 +472,8 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
   long long jn = advance(j);
   long long e = entry(j), en = entry(jn);
   long long jnn = jn < G ? advance(jn) : G;
-  // kStageRegs: the entry after next arrives by cp.async into one of two
-  // per-warp shared slots (the staging area is free then), so no register
+  // NARROW: the entry after next arrives by cp.async into one of two
+  // per-warp shared slots (the first doubles of the warp's scratch), so no register
   // waits for it -- a plain load's result had to be copied into the
   // rotating entry registers right away, and that copy stalled on the load
   // (5 % of the kernel's warp samples)
@@ -500,33 +496,21 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     return v;
   };
   long long enn = 0;
-  if (NARROW && kStageRegs) fetch_entry(jnn);
+  if (NARROW) fetch_entry(jnn);
   else enn = entry(jnn);
   int groups_done = 0;
-  double* s_outT = s_warp + 2 * 3 * 32;   // NARROW: [4][32]
+  double* s_outT = s_warp + 32;   // NARROW: [4][32] (s_warp[0..1]: group entry slots)
   double* s_outQ = s_outT + kGroupCols * 32;
   double* s_term = NARROW ? s_outQ + kGroupCols * 32 : s_warp;   // NARROW: [4][32]; wide: [L]
-  // NARROW: per-lane cp.async staging of the next column into a double
-  // buffer (each lane copies s into its own slot) -- no registers, no
-  // register scoreboard shared with the column's other loads
-  int buf = 0;
-  const unsigned st_addr = opaque_u32(smem_u32(s_warp + lane));
   // this lane's level rows (lane < L)
   const double* T_row = a.T + (long long)min(lane, L - 1) * a.ld_in;
   const double* q_row = a.q + (long long)min(lane, L - 1) * a.ld_in;
   double* outT_row = a.tend_T + (long long)min(lane, L - 1) * a.ld_out;
   double* outQ_row = a.tend_q + (long long)min(lane, L - 1) * a.ld_out;
-  auto stage = [&](long long cc, int b) {
-    const unsigned d = st_addr + b * 768;
-    cp_async8_u32(d, a.s + cc);
-    if (lane < L) {
-      cp_async8_u32(d + 256, T_row + cc);
-      cp_async8_u32(d + 512, q_row + cc);
-    }
-    cp_async_commit();
-  };
-  // kStageRegs: the next column's (s, T[lane], q[lane]) are prefetched into
-  // registers with read-only loads instead of cp.async into shared memory
+  // NARROW: the next column's (s, T[lane], q[lane]) are prefetched into
+  // registers with read-only loads during the current column (cp.async
+  // staging into shared memory measured the same and cost LDGSTS bank
+  // conflicts)
   double nx_s = 0.0, nx_T = 0.0, nx_q = 0.0;
   auto prefetch = [&](long long cc) {
     nx_s = __ldg(a.s + cc);
@@ -541,10 +525,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
   int i = __ffs(rem) - 1;
   rem &= rem - 1;
   long long c = g * kGroupCols + i;
-  if (NARROW) {
-    if (kStageRegs) prefetch(c);
-    else stage(c, 0);
-  }
+  if (NARROW) prefetch(c);
   for (;;) {
     CVG_PCLK(ph0);
     // the column after this one: the group's next, or the next group's first
@@ -552,7 +533,7 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     if (rem) cn = g * kGroupCols + (__ffs(rem) - 1);
     else if (en >= 0) cn = (en >> 4) * kGroupCols + (__ffs((unsigned)(en & 15)) - 1);
     double sc, T_c = 0.0, q_c = 0.0;
-    if (NARROW && kStageRegs) {
+    if (NARROW) {
       sc = nx_s;
       T_c = nx_T;
       q_c = nx_q;
@@ -565,24 +546,6 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       }
 #endif
       if (cn >= 0) prefetch(cn);
-    } else if (NARROW) {
-      cp_async_wait_all();
-      const unsigned d = st_addr + buf * 768;
-      sc = lds_f64(d);
-      if (lane < L) {
-        T_c = lds_f64(d + 256);
-        q_c = lds_f64(d + 512);
-      }
-#ifdef CVG_PHASE_CLOCKS
-      {
-        double chk = sc + T_c + q_c;   // force the staged values here
-        asm volatile("" : "+d"(chk));
-        CVG_PCLK(phw);
-        CVG_PACC(6, ph0, phw);   // wait for the staged column
-      }
-#endif
-      if (cn >= 0) stage(cn, buf ^ 1);
-      buf ^= 1;
     } else {
       sc = a.s[c];
     }
@@ -712,11 +675,11 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
       if (en < 0) break;
       // next group; load the entry after it
       e = en;
-      en = (NARROW && kStageRegs) ? take_entry() : enn;
+      en = NARROW ? take_entry() : enn;
       j = jn;
       jn = jnn;
       jnn = jn < G ? advance(jn) : G;
-      if (NARROW && kStageRegs) fetch_entry(jnn);
+      if (NARROW) fetch_entry(jnn);
       else enn = entry(jnn);
       g = e >> 4;
       m = (unsigned)(e & 15);
