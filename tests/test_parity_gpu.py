@@ -295,3 +295,21 @@ def test_thread_per_column_ragged_and_errors(tpc_ctx, n):
         with pytest.raises(P.KernelError) as e:
             tpc_ctx.deep_convection(s2, T2, q)
         assert e.value.column == n - 2
+
+
+@pytest.mark.parametrize("variant,strict", [(1, False), (2, False), (0, True)])
+def test_full_grid_variants_and_strict(ctx, variant, strict):
+    """The f02 grid through the default (size-switched: thread-per-column)
+    deep kernel for StrengthReduced, ApproxTranscendental (bit-exact work and
+    k-order precip) and the strict update, every 7th column against the
+    oracle."""
+    s, T, q = G.make_config("c4", seed=42)
+    deep, _ = ctx.convect(s, T, q, P.KernelOptions(variant=variant, strict=strict), kernels=P.DEEP)
+    idx = np.arange(0, s.size, 7)
+    sub = lambda a: np.ascontiguousarray(a[..., idx])
+    od = O.convection("deep", sub(s), sub(T), sub(q), O.Options(variant=variant))
+    pick = P.ColumnOutputs(deep.tend_T[:, idx], deep.tend_q[:, idx], deep.precip[idx], deep.work_units[idx],
+                           deep.exited_early[idx])
+    check(pick, od, "deep", bitexact_work=(variant == 2))
+    if variant == 2:
+        assert np.array_equal(pick.precip.view(np.int64), od.precip.view(np.int64))
