@@ -178,9 +178,7 @@ struct cvg_context {
   unsigned long long* h_aux_err = nullptr;
   // tuning switches (environment, read at context creation)
   bool overlap = true;     // CVG_OVERLAP: deep || shallow on two streams
-  int shallow_mode = 0;    // CVG_SHALLOW_MODE: 0 thread per column, 2 TMA-staged tiles
   int deep_warps = 0;      // CVG_DEEP_WARPS: 12, 16 or 20 warps per deep block (0: by mode)
-  bool fused = false;      // CVG_FUSED: shallow tiles inside the deep kernel (L <= 32)
   int shallow_minb = 8;    // CVG_SHALLOW_MINB: shallow blocks per SM the register budget targets (8, 12, 16)
   bool strict = false;     // CVG_STRICT: reference rounding in every Newton update (all variants)
   // CVG_CARVEOUT: shared-memory carveout (% of the 228 KB maximum) preferred
@@ -269,17 +267,16 @@ static int far_window_limit(double tol, bool enabled) {
 static bool aligned32(const void* p) { return ((uintptr_t)p & 31) == 0; }
 
 // Shared memory of one deep block: both exp tables and the per-warp scratch.
-template <int VAR, bool NARROW, int NW, bool FUSED = false, bool SH = true, bool RELAX_SH = false>
-void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st,
-                   const cvg::ShallowArgs& b = cvg::ShallowArgs{}) {
+template <int VAR, bool NARROW, int NW>
+void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
   const int threads = NW * 32;
   const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
                       (size_t)cvg::kExpTableSize * cvg::kTab1Copies * sizeof(double) +
                       (size_t)NW * cvg::deep_warp_doubles(NARROW, a.L) * sizeof(double);
-  auto kern = cvg::deep_kernel<VAR, NARROW, NW, FUSED, SH, RELAX_SH>;
+  auto kern = cvg::deep_kernel<VAR, NARROW, NW>;
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
-  kern<<<ctx->num_sms, threads, smem, st>>>(a, b);
+  kern<<<ctx->num_sms, threads, smem, st>>>(a);
   CVG_CUDA(cudaGetLastError());
 }
 
@@ -289,18 +286,6 @@ void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st,
 template <int VAR>
 void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh,
                     bool dp, cudaEvent_t* pe, cudaStream_t st, bool strict) {
-  if (ctx->fused && dp && a.L <= 32) {
-    // one kernel: deep groups with shallow tiles interleaved
-    const bool relax = VAR != cvg::kVarApprox && !strict;
-    if (sh && relax) launch_deep_t<VAR, true, 20, true, true, true>(ctx, a, st, b);
-    else if (sh) launch_deep_t<VAR, true, 20, true, true, false>(ctx, a, st, b);
-    else launch_deep_t<VAR, true, 20, true, false, false>(ctx, a, st, b);
-    if (pe) {
-      CVG_CUDA(cudaEventRecord(pe[2], st));
-      CVG_CUDA(cudaEventRecord(pe[3], st));
-    }
-    return;
-  }
   const bool ov = ctx->overlap && dp;
   const cudaStream_t main = st;
   if (ov) CVG_CUDA(cudaEventRecord(w.ev_fork, st));
@@ -342,14 +327,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     CVG_CUDA(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
     st = w.side;
   }
-  if (ctx->shallow_mode == 2 && (b.ld_in % 2) == 0) {
-    const size_t smem = (size_t)cvg::kExpTableSize * sizeof(double2) +
-                        (size_t)2 * 2 * b.L * cvg::kShTile * sizeof(double);
-    auto k = sh && dp ? cvg::shallow_tma_kernel<VAR, true, true>
-                      : sh ? cvg::shallow_tma_kernel<VAR, true, false> : cvg::shallow_tma_kernel<VAR, false, true>;
-    CVG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<ctx->num_sms, cvg::kShTile, smem, st>>>(b);
-  } else {
+  {
     const unsigned blocks = (unsigned)((b.n + cvg::kShallowThreads - 1) / cvg::kShallowThreads);
     const bool relax = VAR != cvg::kVarApprox && !strict;
     void (*k)(cvg::ShallowArgs) = nullptr;
@@ -575,9 +553,7 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_CARVEOUT")) ctx->carveout = atoi(e);
     if (const char* e = getenv("CVG_FAR32")) ctx->far32 = atoi(e) != 0;
     if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
-    if (const char* e = getenv("CVG_FUSED")) ctx->fused = atoi(e) != 0;
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
-    if (const char* e = getenv("CVG_SHALLOW_MODE")) ctx->shallow_mode = atoi(e);
     if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
     if (const char* e = getenv("CVG_SLOTS")) ctx->slots = std::max(1, std::min(kSlots, atoi(e)));
     ctx->trace_path = getenv("CVG_TRACE");

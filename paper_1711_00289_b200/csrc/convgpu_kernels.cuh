@@ -269,11 +269,13 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
       te = fte;
       tp = ftp;
     }
+#ifdef CVG_PHASE_CLOCKS
     {
       CVG_PCLK(pf1);
       const int lane = threadIdx.x & 31;
       CVG_PACC(5, pf0, pf1);   // FP32 far loop
     }
+#endif
     ee = exp_relaxed1(kRC, te, tab1_addr);
     ep = exp_relaxed1(kRC, tp, tab1_addr);
     he = fma(kMC.c001, te, ee - ye);
@@ -294,11 +296,13 @@ __device__ __forceinline__ bool deep_lane_pair(const DeepArgs& a, const double2*
       newton_relaxed_step(tp, ep, hp, yp, tab1_addr);
     } while (--left != 0);
     it = maxit + 1 - max(left, 0);
+#ifdef CVG_PHASE_CLOCKS
     {
       CVG_PCLK(pl1);
       const int lane = threadIdx.x & 31;
       CVG_PACC(4, pl0, pl1);   // relaxed Newton loop
     }
+#endif
     int ie = it, ip = it;
     bool ok = newton_finish<VAR>(a, tab, col, k, ye, te, ee, he, ie);
     if (!newton_finish<VAR>(a, tab, col, a.L + k, yp, tp, ep, hp, ip)) ok = false;
@@ -421,21 +425,9 @@ __host__ __device__ constexpr int deep_warp_doubles(bool narrow, int L) {
 // s_tab points at this lane's copy of the replicated exp table; s_warp is
 // this warp's scratch (deep_warp_doubles), s_gwork / s_gok the group's
 // per-column work counts and success flags.
-// Fused mode (FUSED): between groups the warp also works through 32-column
-// tiles of the shallow scheme (+ deep zero-fill), claimed from a second
-// cursor -- one tile every `every` groups, the rest after the deep list is
-// exhausted -- so the HBM-bound shallow work runs inside the FP64-bound deep
-// kernel's latency shadow instead of competing for SM slots as a second
-// kernel.  tile(t) processes tile t (returns false when t is past the end).
-struct NoTiles {
-  __device__ bool operator()(long long) const { return false; }
-};
-
-template <int VAR, bool NARROW, bool FUSED = false, class Tile = NoTiles>
+template <int VAR, bool NARROW>
 __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_tab, unsigned tab1_addr,
-                                            double* s_warp, int* s_gwork, int* s_gok, double* s_gpr,
-                                            int lane, const Tile& tile = Tile(),
-                                            unsigned long long* tile_cursor = nullptr, int every = 1) {
+                                            double* s_warp, int* s_gwork, int* s_gok, double* s_gpr, int lane) {
   const int L = a.L;
   const long long G = *a.count;
   // Work distribution: warps claim groups from a global cursor (one atomic
@@ -456,15 +448,6 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     claim();
     return r;
   };
-  // fused shallow tiles: the next tile index is claimed a tile ahead
-  long long tile_raw = 0;
-  auto tile_claim = [&]() { if (FUSED && lane == 0) tile_raw = claim_chunk(tile_cursor + lane_op); };
-  auto do_tile = [&]() -> bool {
-    const long long tt = __shfl_sync(0xffffffffu, tile_raw, 0);
-    tile_claim();
-    return tile(tt);
-  };
-  tile_claim();
   auto entry = [&](long long x) -> long long { return x < G ? a.groups[x] : -1; };
   claim();
   long long j = __shfl_sync(0xffffffffu, next_raw, 0);
@@ -498,7 +481,6 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
   long long enn = 0;
   if (NARROW) fetch_entry(jnn);
   else enn = entry(jnn);
-  int groups_done = 0;
   double* s_outT = s_warp + 32;   // NARROW: [4][32] (s_warp[0..1]: group entry slots)
   double* s_outQ = s_outT + kGroupCols * 32;
   double* s_term = NARROW ? s_outQ + kGroupCols * 32 : s_warp;   // NARROW: [4][32]; wide: [L]
@@ -668,10 +650,6 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
         }
       }
       __syncwarp();
-      if (FUSED && ++groups_done >= every) {
-        groups_done = 0;
-        do_tile();
-      }
       if (en < 0) break;
       // next group; load the entry after it
       e = en;
@@ -697,7 +675,6 @@ __device__ __forceinline__ void deep_worker(const DeepArgs& a, const double2* s_
     c = g * kGroupCols + i;
   }
   }   // e >= 0
-  if (FUSED) while (do_tile()) {}
 }
 
 // ---------------------------------------------------------------------------
@@ -759,13 +736,6 @@ struct GlobalRows {
   long long ld;
   __device__ __forceinline__ double t(int k) const { return T[(long long)k * ld]; }
   __device__ __forceinline__ double m(int k) const { return q[(long long)k * ld]; }
-};
-struct SmemRows {
-  const double* T;
-  const double* q;
-  int ld;
-  __device__ __forceinline__ double t(int k) const { return T[k * ld]; }
-  __device__ __forceinline__ double m(int k) const { return q[k * ld]; }
 };
 
 // The deep zero-fill of a column belongs to the shallow kernel only when its
@@ -947,80 +917,14 @@ __global__ void __launch_bounds__(kShallowThreads, MINB) shallow_kernel(ShallowA
 
 // ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
-// Streaming shallow(+zero-fill) kernel on the TMA engine: one persistent
-// block per SM walks tiles of kShTile columns; thread 0 stages the next
-// tile's 2L rows (T and q, 1 KB each) into the idle half of a double buffer
-// with cp.async.bulk while the block computes the current tile out of
-// shared memory, so every SM keeps a whole tile (2 L KB) of loads in flight
-// without registers, and the survivors' output pass re-reads T, q from
-// shared memory instead of HBM.  Requires ld_in % 2 == 0 (16-byte aligned
-// rows); the tail (n % kShTile columns) is done from global by block 0.
-constexpr int kShTile = 128;
-
-template <int VAR, bool DO_SHALLOW, bool DO_DEEP_ZERO>
-__global__ void __launch_bounds__(kShTile, 1) shallow_tma_kernel(ShallowArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t s_bar[2];
-  double2* s_tab = reinterpret_cast<double2*>(smem_raw);                       // 8 KB
-  double* buf = reinterpret_cast<double*>(smem_raw + kExpTableSize * sizeof(double2));
-  const int L = a.L;
-  const int tid = threadIdx.x;
-  const size_t stage_elems = (size_t)2 * L * kShTile;   // T then q, [L][kShTile] each
-  const long long ntiles = a.n / kShTile;
-  if (tid == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
-    fence_mbar_init();
-  }
-  if (DO_SHALLOW && VAR != kVarApprox) {
-    for (int i = tid; i < kExpTableSize; i += blockDim.x) s_tab[i] = a.exp_tab[i];
-  }
-  __syncthreads();
-  auto issue = [&](long long tile, int stage) {
-    double* dT = buf + stage * stage_elems;
-    double* dq = dT + (size_t)L * kShTile;
-    const long long c0 = tile * kShTile;
-    mbar_arrive_expect_tx(&s_bar[stage], (unsigned)(2 * L * kShTile * sizeof(double)));
-    for (int k = 0; k < L; ++k) {
-      bulk_g2s(dT + k * kShTile, a.T + (long long)k * a.ld_in + c0, kShTile * sizeof(double), &s_bar[stage]);
-      bulk_g2s(dq + k * kShTile, a.q + (long long)k * a.ld_in + c0, kShTile * sizeof(double), &s_bar[stage]);
-    }
-  };
-  long long tile = blockIdx.x;
-  if (DO_SHALLOW && tid == 0 && tile < ntiles) issue(tile, 0);
-  for (int i = 0; tile < ntiles; ++i, tile += gridDim.x) {
-    const int stage = i & 1;
-    const long long nxt = tile + gridDim.x;
-    if (DO_SHALLOW && tid == 0 && nxt < ntiles) issue(nxt, stage ^ 1);
-    const long long c = tile * kShTile + tid;
-    const double sc = a.s[c];
-    if (DO_SHALLOW) {
-      mbar_wait_parity(&s_bar[stage], (unsigned)((i >> 1) & 1));
-      const double* sT = buf + stage * stage_elems + tid;
-      shallow_column_src<VAR, true, DO_DEEP_ZERO, 1>(a, c, sc, SmemRows{sT, sT + (size_t)L * kShTile, kShTile},
-                                                     s_tab, group_untriggered(sc, a.thr));
-    } else {
-      shallow_column_src<VAR, false, DO_DEEP_ZERO, 1>(a, c, sc, GlobalRows{a.T + c, a.q + c, a.ld_in}, s_tab,
-                                                      group_untriggered(sc, a.thr));
-    }
-    __syncthreads();  // stage fully consumed before it is refilled
-  }
-  if (blockIdx.x == 0) {
-    for (long long c = ntiles * kShTile + tid; c < a.n; c += blockDim.x)
-      shallow_column<VAR, DO_SHALLOW, DO_DEEP_ZERO, 1>(a, c, s_tab);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Persistent deep kernel: one block per SM; every warp works the deep list
 // (deep_worker).  kDeepWarps when it runs alone, kDeepWarpsOverlap when the
 // shallow kernel shares the SMs (convgpu.cu, overlap mode).
 // Measured (f02, 1 B200, grouped sector-wide stores): alone, 20 warps (0.478
 // ms) beat 16 (0.487) and 24 (0.503, register-capped); in overlap mode 12
-// warps (~37K registers) leave room for three 128-thread shallow blocks per
-// SM, enough for the shallow kernel to finish under the deep one (step 0.66
-// ms, against 0.74 at 14 warps and 0.81 at 16, where the shallow blocks
-// starve).
+// warps leave room for three 128-thread shallow blocks per SM, enough for
+// the shallow kernel to finish under the deep one (step 0.66 ms, against
+// 0.74 at 14 warps and 0.81 at 16, where the shallow blocks starve).
 constexpr int kDeepWarps = 20;
 constexpr int kDeepWarpsOverlap = 12;
 
@@ -1035,10 +939,8 @@ constexpr int deep_max_regs() {
   return ((budget / (NW * 32)) & ~7) > 255 ? 255 : ((budget / (NW * 32)) & ~7);
 }
 
-// FUSED: also runs the shallow scheme (SH) or only the deep zero-fill (!SH)
-// over 32-column tiles (see deep_worker); b.trace unused.
-template <int VAR, bool NARROW, int NW, bool FUSED = false, bool SH = true, bool RELAX_SH = false>
-__global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a, ShallowArgs b) {
+template <int VAR, bool NARROW, int NW>
+__global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
 #ifdef CVG_PHASE_CLOCKS
   if (threadIdx.x < 8) s_phase[threadIdx.x] = 0;
@@ -1067,21 +969,7 @@ __global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a, Shallow
   // rematerialised from %tid inside the Newton loop
   const unsigned tab1_addr = opaque_u32(smem_u32(s_tab1_all + (lane & (kTab1Copies - 1))));
   double* s_warp = s_tab1_all + kExpTableSize * kTab1Copies + (size_t)wib * deep_warp_doubles(NARROW, a.L);
-  if (FUSED) {
-    const long long ntiles = (b.n + 31) / 32;
-    const long long G = *a.count;
-    const int every = (int)max(1LL, G / max(1LL, ntiles));
-    auto tile = [&](long long tt) -> bool {
-      if (tt >= ntiles) return false;
-      const long long c = tt * 32 + lane;
-      if (c < b.n) shallow_column<VAR, SH, true, 1, RELAX_SH>(b, c, s_tab_all);
-      return true;
-    };
-    deep_worker<VAR, NARROW, true>(a, s_tab, tab1_addr, s_warp, s_gwork[wib], s_gok[wib], s_gpr[wib], lane, tile,
-                                   a.cursor + 16, every);
-  } else {
-    deep_worker<VAR, NARROW>(a, s_tab, tab1_addr, s_warp, s_gwork[wib], s_gok[wib], s_gpr[wib], lane);
-  }
+  deep_worker<VAR, NARROW>(a, s_tab, tab1_addr, s_warp, s_gwork[wib], s_gok[wib], s_gpr[wib], lane);
 #ifdef CVG_PHASE_CLOCKS
   __syncthreads();
   if (threadIdx.x < 8) atomicAdd(&g_phase[threadIdx.x], s_phase[threadIdx.x]);
