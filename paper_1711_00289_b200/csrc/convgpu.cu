@@ -211,6 +211,7 @@ struct cvg_context {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
+  int deep_lpc = -1;          // CVG_DEEP_LPC: lanes per column for calls under kTpcMinColumns (-1 by size, 0 off, 2, 4)
   int deep_tpc = 2;           // CVG_DEEP_TPC: thread-per-column deep kernel: 0 never, 1 always, 2 for large calls
   // cvg_timestep state, kept across calls (the reference's persistent
   // buffers, hetero.hpp:44)
@@ -296,12 +297,22 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // 0.078 vs 0.089 ms at 8-way).  CVG_DEEP_TPC: 0 never, 1 always, 2 auto.
   const bool tpc = dp && a.L <= 32 &&
                    (ctx->deep_tpc == 1 || (ctx->deep_tpc == 2 && a.n >= cvg::kTpcMinColumns));
-  if (tpc) {
+  // split columns (LPC lanes per column) for smaller calls where the
+  // relaxed path allows the fixed-shape precip sum: shorter claims, the
+  // thread-per-column kernel's per-column economy (f02 shares: 4-way 0.133
+  // ms at LPC 2 vs 0.141 warp-per-column; 8-way max 0.076 at LPC 4 vs
+  // 0.081).  CVG_DEEP_LPC: -1 by size (default), 0 off, 2 or 4 forced.
+  const int lpc_n = ctx->deep_lpc >= 0 ? ctx->deep_lpc : (a.n >= cvg::kTpcMinColumns / 2 ? 2 : 4);
+  const bool lpc = !tpc && dp && a.L <= 32 && a.tree_precip && lpc_n > 1;
+  if (tpc || lpc) {
     const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
                         (size_t)cvg::kExpTableSize * cvg::kTab1Copies * sizeof(double);
     // beside the shallow kernel: one 12-warp block per SM (registers capped
     // so three shallow blocks fit); alone: two 10-warp blocks per SM
-    auto kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
+    void (*kern)(cvg::DeepArgs) = nullptr;
+    if (tpc) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
+    else if (lpc_n == 2) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104, 2> : cvg::deep_tpc_kernel<VAR, 10, 96, 2>;
+    else kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104, 4> : cvg::deep_tpc_kernel<VAR, 10, 96, 4>;
     const int nwt = ov ? 12 : 10, blocks = ov ? 1 : 2;
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
@@ -549,6 +560,7 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_STRICT")) ctx->strict = atoi(e) != 0;
     if (const char* e = getenv("CVG_GRAPH")) ctx->use_graphs = atoi(e) != 0;
     if (const char* e = getenv("CVG_DEEP_TPC")) ctx->deep_tpc = atoi(e);
+    if (const char* e = getenv("CVG_DEEP_LPC")) ctx->deep_lpc = atoi(e);
     if (const char* e = getenv("CVG_RESET_KERNEL")) ctx->reset_kernel = atoi(e) != 0;
     if (const char* e = getenv("CVG_CARVEOUT")) ctx->carveout = atoi(e);
     if (const char* e = getenv("CVG_FAR32")) ctx->far32 = atoi(e) != 0;

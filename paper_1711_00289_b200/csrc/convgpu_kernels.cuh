@@ -990,8 +990,14 @@ __global__ void __maxnreg__(deep_max_regs<NW>()) deep_kernel(DeepArgs a) {
 // Calls with at least this many columns use it (convgpu.cu launch_kernels).
 constexpr long long kTpcMinColumns = 320000;
 
-template <int VAR, int NW, int REGCAP>
+// LPC lanes per column (1: one thread per column; 2, 4: a column's levels
+// split round-robin over LPC lanes -- shorter claims for small calls, the
+// precip then a fixed-shape sum over the LPC lanes' k-ordered partial sums,
+// so LPC > 1 is used only where tree_precip is allowed).
+template <int VAR, int NW, int REGCAP, int LPC = 1>
 __global__ void __maxnreg__(REGCAP) deep_tpc_kernel(DeepArgs a) {
+  constexpr int kCols = 32 / LPC;              // columns per warp claim
+  constexpr int kGroupsPerClaim = kCols / kGroupCols;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (a.trace && threadIdx.x == 0) {
     a.trace[3 * blockIdx.x] = smid();
@@ -1007,6 +1013,7 @@ __global__ void __maxnreg__(REGCAP) deep_tpc_kernel(DeepArgs a) {
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  const int cs = lane / LPC, sub = lane % LPC;   // column slot, level phase
   const double2* s_tab = s_tab_all + (lane & (kTabCopies - 1));
   const unsigned tab1_addr = opaque_u32(smem_u32(s_tab1_all + (lane & (kTab1Copies - 1))));
   const long long G = *a.count;
@@ -1014,59 +1021,74 @@ __global__ void __maxnreg__(REGCAP) deep_tpc_kernel(DeepArgs a) {
   const unsigned lane_op = opaque_u32(lane);
   for (;;) {
     long long j = 0;
-    if (lane == 0) j = (long long)atomicAdd(a.cursor + lane_op, 8ULL);
+    if (lane == 0) j = (long long)atomicAdd(a.cursor + lane_op, (unsigned long long)kGroupsPerClaim);
     j = __shfl_sync(0xffffffffu, j, 0);
     if (j >= G) break;
-    const long long x = j + (lane >> 2);
+    const long long x = j + cs / kGroupCols;
     const long long e = x < G ? a.groups[x] : -1;
-    const int slot = lane & 3;
+    const int slot = cs & (kGroupCols - 1);
     const long long c = e >= 0 ? (e >> 4) * kGroupCols + slot : -1;
-    if (c < 0 || c >= a.n) continue;
-    const bool trig = (e >> slot) & 1;
-    double* pT = a.tend_T + c;
-    double* pQ = a.tend_q + c;
-    if (!trig) {
-      for (int k = 0; k < L; ++k) {
-        pT[(long long)k * a.ld_out] = 0.0;
-        pQ[(long long)k * a.ld_out] = 0.0;
-      }
-      a.precip[c] = 0.0;
-      a.work[c] = 0;
-      a.exited[c] = 1;
-      continue;
-    }
-    const double sc = a.s[c];
-    const double guess = add(24.0, mul(160.0, sc));
-    const double rho = add(1.0, mul(kMC.c005, sc));
-    const double e0 = deep_exp<VAR>(mul(kMC.c005, guess), s_tab);
-    const double c0 = add(e0, mul(kMC.c001, guess));
-    const bool col_far = guess < 512.0;
-    const double* Tr = a.T + c;
-    const double* qr = a.q + c;
+    const bool valid = c >= 0 && c < a.n;
+    const bool trig = valid && ((e >> slot) & 1);
     double pr = 0.0;
     long long wsum = 0;
     bool ok = true;
-    double Tn = __ldg(Tr), qn = __ldg(qr);
-    for (int k = 0; k < L; ++k) {
-      const double T = Tn, q = qn;
-      if (k + 1 < L) {
-        Tn = __ldg(Tr + (long long)(k + 1) * a.ld_in);
-        qn = __ldg(qr + (long long)(k + 1) * a.ld_in);
+    if (valid && !trig) {
+      for (int k = sub; k < L; k += LPC) {
+        a.tend_T[(long long)k * a.ld_out + c] = 0.0;
+        a.tend_q[(long long)k * a.ld_out + c] = 0.0;
       }
-      double tT, tq, term;
-      int w;
-      if (!deep_level<VAR>(a, s_tab, tab1_addr, a.first_col + c, k, sc, rho, guess, e0, c0, col_far, T, q, tT,
-                           tq, term, w))
-        ok = false;
-      pT[(long long)k * a.ld_out] = tT;
-      pQ[(long long)k * a.ld_out] = tq;
-      pr = add(pr, term);   // physics.cpp:161, k order
-      wsum += w;
+    } else if (trig) {
+      double* pT = a.tend_T + c;
+      double* pQ = a.tend_q + c;
+      const double sc = a.s[c];
+      const double guess = add(24.0, mul(160.0, sc));
+      const double rho = add(1.0, mul(kMC.c005, sc));
+      const double e0 = deep_exp<VAR>(mul(kMC.c005, guess), s_tab);
+      const double c0 = add(e0, mul(kMC.c001, guess));
+      const bool col_far = guess < 512.0;
+      const double* Tr = a.T + c;
+      const double* qr = a.q + c;
+      double Tn = 0.0, qn = 0.0;
+      if (sub < L) {
+        Tn = __ldg(Tr + (long long)sub * a.ld_in);
+        qn = __ldg(qr + (long long)sub * a.ld_in);
+      }
+      for (int k = sub; k < L; k += LPC) {
+        const double T = Tn, q = qn;
+        if (k + LPC < L) {
+          Tn = __ldg(Tr + (long long)(k + LPC) * a.ld_in);
+          qn = __ldg(qr + (long long)(k + LPC) * a.ld_in);
+        }
+        double tT, tq, term;
+        int w;
+        if (!deep_level<VAR>(a, s_tab, tab1_addr, a.first_col + c, k, sc, rho, guess, e0, c0, col_far, T, q, tT,
+                             tq, term, w))
+          ok = false;
+        pT[(long long)k * a.ld_out] = tT;
+        pQ[(long long)k * a.ld_out] = tq;
+        pr = add(pr, term);   // physics.cpp:161, k order (within the lane's levels)
+        wsum += w;
+      }
     }
-    if (ok) {
-      a.precip[c] = pr;
-      a.work[c] = wsum;
-      a.exited[c] = 0;
+    if (LPC > 1) {   // combine the column's lanes (fixed shape)
+#pragma unroll
+      for (int o = LPC / 2; o > 0; o >>= 1) {
+        pr = add(pr, __shfl_xor_sync(0xffffffffu, pr, o));
+        wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+        ok = __shfl_xor_sync(0xffffffffu, (int)ok, o) && ok;
+      }
+    }
+    if (sub == 0 && valid) {
+      if (!trig) {
+        a.precip[c] = 0.0;
+        a.work[c] = 0;
+        a.exited[c] = 1;
+      } else if (ok) {
+        a.precip[c] = pr;
+        a.work[c] = wsum;
+        a.exited[c] = 0;
+      }
     }
   }
   if (a.trace) {

@@ -22,16 +22,15 @@ MEAN_UPDATES = 694.0
 BYTES_PER_COLUMN_30 = 1482.0
 
 # Measured per-unit step times on one B200 at L = 30 (the analogue of the
-# reference's calibrate(), hetero.cpp:110-163): a least-squares fit of the
-# f02 step over its 1/4/8-way shares (bench.py --slice R/W) gives
-# t = 22 us + 1.34 ns per triggered column + 0.155 ns per column; a further
-# hand refit of the ratio on the per-rank times (deep-heavy shares run
-# their tail with the shallow kernel gone and only the overlap-size deep
-# blocks, so they cost more than linear) settles at 11: a triggered column
-# weighs 11 plain columns (the FLOP/byte model says 4.0), giving per-rank
-# times within 6 % of each other at 8 ranks and 7 % at 4.
-MEASURED_NS_PER_TRIGGERED = 1.45
-MEASURED_NS_PER_COLUMN = 0.132
+# reference's calibrate(), hetero.cpp:110-163), refit whenever the kernels
+# change: a least-squares fit of the f02 step over its 4- and 8-way shares
+# (bench.py --slice R/W; split-column deep kernel at these sizes) gives
+# t = 19 us + 0.83 ns per triggered column + 0.23 ns per column -- a
+# triggered column weighs ~4 plain columns.  (With the warp-per-column deep
+# kernel the ratio was 11: its deep-heavy shares ran their tail with few
+# warps; the split-column kernel's short claims removed that.)
+MEASURED_NS_PER_TRIGGERED = 0.83
+MEASURED_NS_PER_COLUMN = 0.21
 
 
 def partition_weights(L: int = 30, hbm_gbs: float = 6558.7, fp64_tflops: float = 34.0, mode: str = "balanced"):

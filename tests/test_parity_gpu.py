@@ -313,3 +313,26 @@ def test_full_grid_variants_and_strict(ctx, variant, strict):
     check(pick, od, "deep", bitexact_work=(variant == 2))
     if variant == 2:
         assert np.array_equal(pick.precip.view(np.int64), od.precip.view(np.int64))
+
+
+@pytest.fixture(scope="module", params=[("0", "0"), ("0", "2")], ids=["warp_per_column", "lpc2"])
+def kernel_ctx(request):
+    """Deep kernels the size switch does not pick at test sizes: the
+    warp-per-column kernel on the relaxed path (CVG_DEEP_LPC=0) and the
+    2-lanes-per-column split (CVG_DEEP_LPC=2)."""
+    from conftest import env_context
+    tpc, lpc = request.param
+    c = env_context(CVG_DEEP_TPC=tpc, CVG_DEEP_LPC=lpc)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("cfg,kw", CONFIGS, ids=[c for c, _ in CONFIGS])
+def test_other_deep_kernels_match_oracle(kernel_ctx, cfg, kw, variant):
+    s, T, q = G.make_config(cfg, seed=19, **kw)
+    thr = G.config_threshold(cfg)
+    deep, sh = kernel_ctx.convect(s, T, q, P.KernelOptions(variant=variant, activity_threshold=thr))
+    oo = O.Options(variant=variant, activity_threshold=thr)
+    check(deep, O.convection("deep", s, T, q, oo), "deep")
+    check(sh, O.convection("shallow", s, T, q, oo), "shallow")
