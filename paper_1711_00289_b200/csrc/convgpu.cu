@@ -295,15 +295,19 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // share; its 32-column claims take ~90 us per warp, so from 4-way shares
   // down the warp-per-column kernel's finer claims win (0.138 vs 0.152 ms,
   // 0.078 vs 0.089 ms at 8-way).  CVG_DEEP_TPC: 0 never, 1 always, 2 auto.
-  const bool tpc = dp && a.L <= 32 &&
-                   (ctx->deep_tpc == 1 || (ctx->deep_tpc == 2 && a.n >= cvg::kTpcMinColumns));
-  // split columns (LPC lanes per column) for smaller calls where the
-  // relaxed path allows the fixed-shape precip sum: shorter claims, the
-  // thread-per-column kernel's per-column economy (f02 shares: 4-way 0.133
-  // ms at LPC 2 vs 0.141 warp-per-column; 8-way max 0.076 at LPC 4 vs
-  // 0.081).  CVG_DEEP_LPC: -1 by size (default), 0 off, 2 or 4 forced.
+  // Deep kernel by call: on the relaxed path (fixed-shape precip sums
+  // allowed) the split-column kernel, 2 lanes per column from 160k columns
+  // (f02: 0.434 ms step against 0.452 thread-per-column and 0.508
+  // warp-per-column), 4 below (shorter claims for small shares); otherwise
+  // (strict, ApproxTranscendental: k-order precip) one thread per column
+  // for calls of >= 320k columns, the warp-per-column kernel below.
+  // CVG_DEEP_TPC=1 forces one thread per column, CVG_DEEP_LPC=0 turns the
+  // split off, CVG_DEEP_LPC=2/4 forces its width.
+  const bool tpc_forced = ctx->deep_tpc == 1;
   const int lpc_n = ctx->deep_lpc >= 0 ? ctx->deep_lpc : (a.n >= cvg::kTpcMinColumns / 2 ? 2 : 4);
-  const bool lpc = !tpc && dp && a.L <= 32 && a.tree_precip && lpc_n > 1;
+  const bool lpc = !tpc_forced && dp && a.L <= 32 && a.tree_precip && lpc_n > 1;
+  const bool tpc = !lpc && dp && a.L <= 32 &&
+                   (tpc_forced || (ctx->deep_tpc == 2 && a.n >= cvg::kTpcMinColumns));
   if (tpc || lpc) {
     const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
                         (size_t)cvg::kExpTableSize * cvg::kTab1Copies * sizeof(double);
