@@ -336,3 +336,18 @@ def test_other_deep_kernels_match_oracle(kernel_ctx, cfg, kw, variant):
     oo = O.Options(variant=variant, activity_threshold=thr)
     check(deep, O.convection("deep", s, T, q, oo), "deep")
     check(sh, O.convection("shallow", s, T, q, oo), "shallow")
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 1001])
+def test_other_deep_kernels_ragged_and_errors(kernel_ctx, n):
+    s, T, q = G.make_config("c1", n=n, seed=6)
+    deep, _ = kernel_ctx.convect(s, T, q)
+    check(deep, O.convection("deep", s, T, q), "deep")
+    if n >= 7:
+        s2 = np.full_like(s, 0.9)
+        T2 = T.copy()
+        T2[11, n - 1] = np.nan
+        T2[2, n - 3] = np.nan
+        with pytest.raises(P.KernelError) as e:
+            kernel_ctx.deep_convection(s2, T2, q)
+        assert e.value.column == n - 3
