@@ -315,8 +315,12 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     // so three shallow blocks fit); alone: two 10-warp blocks per SM
     void (*kern)(cvg::DeepArgs) = nullptr;
     if (tpc) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
-    else if (lpc_n == 2) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104, 2> : cvg::deep_tpc_kernel<VAR, 10, 96, 2>;
-    else kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104, 4> : cvg::deep_tpc_kernel<VAR, 10, 96, 4>;
+    // the split kernels are capped at 80 registers beside the shallow kernel
+    // (79 used, no spills): room for a fourth shallow block per SM, which
+    // the shallow kernel -- the step's tail -- turns into speed (f02 0.435
+    // -> 0.420 ms; 8-way max share 0.078 -> 0.072 ms)
+    else if (lpc_n == 2) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 2> : cvg::deep_tpc_kernel<VAR, 10, 96, 2>;
+    else kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 4> : cvg::deep_tpc_kernel<VAR, 10, 96, 4>;
     const int nwt = ov ? 12 : 10, blocks = ov ? 1 : 2;
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
