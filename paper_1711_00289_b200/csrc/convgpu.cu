@@ -295,17 +295,16 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // share; its 32-column claims take ~90 us per warp, so from 4-way shares
   // down the warp-per-column kernel's finer claims win (0.138 vs 0.152 ms,
   // 0.078 vs 0.089 ms at 8-way).  CVG_DEEP_TPC: 0 never, 1 always, 2 auto.
-  // Deep kernel by call: on the relaxed path (fixed-shape precip sums
-  // allowed) the split-column kernel, 2 lanes per column from 160k columns
-  // (f02: 0.434 ms step against 0.452 thread-per-column and 0.508
-  // warp-per-column), 4 below (shorter claims for small shares); otherwise
-  // (strict, ApproxTranscendental: k-order precip) one thread per column
-  // for calls of >= 320k columns, the warp-per-column kernel below.
-  // CVG_DEEP_TPC=1 forces one thread per column, CVG_DEEP_LPC=0 turns the
-  // split off, CVG_DEEP_LPC=2/4 forces its width.
+  // Deep kernel by call: the split-column kernel, 2 lanes per column from
+  // 160k columns (f02: 0.420 ms step against 0.452 with one thread per
+  // column and 0.508 warp-per-column), 4 below (shorter claims for small
+  // shares); every variant (precip in k order, or on the relaxed path a
+  // fixed-shape sum of the lanes' k-ordered partials).  CVG_DEEP_TPC=1 forces one
+  // thread per column, CVG_DEEP_LPC=0 the warp-per-column kernel,
+  // CVG_DEEP_LPC=2/4 the split width.
   const bool tpc_forced = ctx->deep_tpc == 1;
   const int lpc_n = ctx->deep_lpc >= 0 ? ctx->deep_lpc : (a.n >= cvg::kTpcMinColumns / 2 ? 2 : 4);
-  const bool lpc = !tpc_forced && dp && a.L <= 32 && a.tree_precip && lpc_n > 1;
+  const bool lpc = !tpc_forced && dp && lpc_n > 1;
   const bool tpc = !lpc && dp && a.L <= 32 &&
                    (tpc_forced || (ctx->deep_tpc == 2 && a.n >= cvg::kTpcMinColumns));
   if (tpc || lpc) {
@@ -319,8 +318,13 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     // (79 used, no spills): room for a fourth shallow block per SM, which
     // the shallow kernel -- the step's tail -- turns into speed (f02 0.435
     // -> 0.420 ms; 8-way max share 0.078 -> 0.072 ms)
-    else if (lpc_n == 2) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 2> : cvg::deep_tpc_kernel<VAR, 10, 96, 2>;
-    else kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 4> : cvg::deep_tpc_kernel<VAR, 10, 96, 4>;
+    else if (a.tree_precip) {
+      if (lpc_n == 2) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 2, false> : cvg::deep_tpc_kernel<VAR, 10, 96, 2, false>;
+      else kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 4, false> : cvg::deep_tpc_kernel<VAR, 10, 96, 4, false>;
+    } else {
+      if (lpc_n == 2) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 2> : cvg::deep_tpc_kernel<VAR, 10, 96, 2>;
+      else kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 4> : cvg::deep_tpc_kernel<VAR, 10, 96, 4>;
+    }
     const int nwt = ov ? 12 : 10, blocks = ov ? 1 : 2;
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
