@@ -241,7 +241,11 @@ def run_gpu_arm(args):
     from paper_1711_00289_b200 import gridgen
 
     ws, rank, local = dist_env()
-    dist = init_dist(ws, "nccl")
+    # BENCH_DIST_BACKEND / BENCH_DEVICE: functional check of the N > 1 path
+    # on a one-GPU box (every rank on one device, gloo) -- not a measurement
+    dist = init_dist(ws, os.environ.get("BENCH_DIST_BACKEND", "nccl"))
+    if os.environ.get("BENCH_DEVICE") is not None:
+        local = int(os.environ["BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -414,8 +418,12 @@ def run_gpu_arm(args):
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te[0])
-        e2e = {"value": n_total * Ke / el, "unit": UNIT, "h2d_bytes_per_step": int(stt.h2d_bytes),
-               "d2h_bytes_per_step": int(stt.d2h_bytes), "steps": Ke,
+        # bytes moved per step by the whole job (all ranks)
+        tb = torch.tensor([float(stt.h2d_bytes), float(stt.d2h_bytes)], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+        e2e = {"value": n_total * Ke / el, "unit": UNIT, "h2d_bytes_per_step": int(tb[0]),
+               "d2h_bytes_per_step": int(tb[1]), "steps": Ke,
                "ms_per_step": 1e3 * el / Ke,
                "note": "cvg_convect (C ABI) on pinned host SoA buffers: H2D inputs, compute, D2H all outputs, per step; wall clock, max over ranks"}
         for a in pin + pdo + pso:
