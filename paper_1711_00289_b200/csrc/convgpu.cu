@@ -697,7 +697,11 @@ cvg_status cvg_convect_async(cvg_context* ctx, const cvg_columns* in, const cvg_
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     cudaEvent_t* pe = nullptr;
     if (ctx->prof_on && ctx->prof_n < ctx->prof_cap) pe = &ctx->prof_ev[4 * ctx->prof_n++];
-    if (pe || ctx->trace_path || !ctx->use_graphs || in->n_columns == 0) {
+    // a caller capturing its own graph on this stream gets the plain
+    // launches recorded into it (no nested capture)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CVG_CUDA(cudaStreamIsCapturing(st, &cap));
+    if (pe || ctx->trace_path || !ctx->use_graphs || in->n_columns == 0 || cap != cudaStreamCaptureStatusNone) {
       enqueue(ctx, ctx->ws[0], in, opts, mask, deep, sh, st, pe);
     } else {
       launch_graph(ctx, in, opts, mask, deep, sh, st);

@@ -334,3 +334,31 @@ def test_option_flags(ctx):
     od = O.convection("deep", s, T, q)
     both_close(a, od)
     both_close(b, od)
+
+
+def test_async_call_inside_a_caller_graph(ctx):
+    """convect_async recorded into the caller's own CUDA graph (torch
+    capture) and replayed matches a direct call."""
+    import torch
+    dev = torch.device("cuda", 0)
+    s, T, q = G.make_config("c2", n=4096, seed=31)
+    L, n = T.shape
+    ds, dT, dq = (torch.from_numpy(a).to(dev) for a in (s, T, q))
+
+    def outs():
+        return (torch.zeros((L, n), dtype=torch.float64, device=dev), torch.zeros((L, n), dtype=torch.float64, device=dev),
+                torch.zeros(n, dtype=torch.float64, device=dev), torch.zeros(n, dtype=torch.int64, device=dev),
+                torch.zeros(n, dtype=torch.uint8, device=dev))
+    do, so = outs(), outs()
+    st = torch.cuda.Stream()
+    ctx.convect_async(ds, dT, dq, do, so, stream=st)   # warm (workspace sized)
+    ctx.check(st)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        ctx.convect_async(ds, dT, dq, do, so, stream=st)
+    for t in do + so:
+        t.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in do]), O.convection("deep", s, T, q))
+    both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in so]), O.convection("shallow", s, T, q))
