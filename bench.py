@@ -507,7 +507,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=["ref", "c1", "c2", "c3", "c4", "c5_05", "c5_50", "c5_95"])
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--seed", type=int, default=42)
-    ap.add_argument("--partition", default="balanced", choices=["balanced", "model", "naive"])
+    ap.add_argument("--partition", default="balanced", choices=["balanced", "overlap", "model", "naive"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-loop", action="store_true", help="skip the feedback-loop measurement")

@@ -54,10 +54,57 @@ def rank_bounds(s, activity_threshold: float, world: int, mode: str = "balanced"
     at most 16 columns per boundary)."""
     if mode == "naive":
         b = plan_partition(s, activity_threshold, world, 0.0, 1.0)
+    elif mode == "overlap":
+        b = overlap_bounds(s, activity_threshold, world, L)
     else:
         dw, sw = partition_weights(L, hbm_gbs, fp64_tflops, mode)
         b = plan_partition(s, activity_threshold, world, dw, sw)
     return align_bounds(b, ALIGN)
+
+
+# Overlap-aware share cost (the deep and shallow kernels run concurrently):
+# t = C0 + max(D, S) + GAMMA * min(D, S), D = A_DEEP * triggered columns,
+# S = B_SHALLOW * columns -- a deep-bound share hides most of its shallow
+# work and vice versa.  Fit on one B200: all-triggered c5_50 shares (deep
+# bound), its mixed shares (shallow bound) and the f02 step (GAMMA).
+C0_MS, A_DEEP_MS, B_SHALLOW_MS, GAMMA = 0.019, 1.29e-6, 0.27e-6, 0.25
+
+
+def share_cost(n_trig, n_cols):
+    d, sh = A_DEEP_MS * n_trig, B_SHALLOW_MS * n_cols
+    return C0_MS + np.maximum(d, sh) + GAMMA * np.minimum(d, sh)
+
+
+def overlap_bounds(s, activity_threshold: float, world: int, L: int = 30) -> np.ndarray:
+    """Contiguous ranges minimising the largest share_cost: bisection on the
+    target cost, each rank taking the longest prefix within it (the cost of
+    a range grows with its end)."""
+    n = int(np.asarray(s).size)
+    trig = np.concatenate([[0], np.cumsum(np.asarray(s) > activity_threshold)]).astype(np.int64)
+    scale = L / 30.0
+
+    def greedy(target):
+        b = [0]
+        for _ in range(world - 1):
+            lo = b[-1]
+            ends = np.arange(lo, n + 1)
+            c = scale * share_cost(trig[ends] - trig[lo], ends - lo)
+            k = int(np.searchsorted(c > target, True))   # first end over the target
+            b.append(lo + max(k - 1, 0))
+        b.append(n)
+        return np.array(b, dtype=np.int64)
+
+    def worst(b):
+        return max(scale * share_cost(trig[b[i + 1]] - trig[b[i]], b[i + 1] - b[i]) for i in range(world))
+
+    lo_t, hi_t = 0.0, float(scale * share_cost(trig[n], n))
+    for _ in range(40):
+        mid = 0.5 * (lo_t + hi_t)
+        if worst(greedy(mid)) <= mid + 1e-12 and greedy(mid)[-2] <= n:
+            hi_t = mid
+        else:
+            lo_t = mid
+    return greedy(hi_t)
 
 
 ALIGN = 32
