@@ -94,7 +94,7 @@ def test_partition_bounds_are_aligned_and_monotone():
     from paper_1711_00289_b200 import gridgen, multigpu
     s, _, _ = gridgen.make_config("c5_50", shape=(48, 64), seed=4)
     for world in (1, 2, 3, 8):
-        for mode in ("balanced", "model", "naive"):
+        for mode in ("balanced", "overlap", "model", "naive"):
             b = multigpu.rank_bounds(s, 0.5, world, mode)
             assert b[0] == 0 and b[-1] == s.size and len(b) == world + 1
             assert np.all(np.diff(b) >= 0)
@@ -102,3 +102,17 @@ def test_partition_bounds_are_aligned_and_monotone():
     # rounding moves a boundary by at most ALIGN / 2
     raw = P.plan_partition(s, 0.5, 8, *multigpu.partition_weights())
     assert np.max(np.abs(multigpu.align_bounds(raw) - raw)) <= multigpu.ALIGN // 2
+
+
+def test_overlap_partition_minimises_the_largest_share():
+    """overlap_bounds: no share's modelled cost exceeds the linear split's
+    worst share (the bisection minimises the maximum)."""
+    from paper_1711_00289_b200 import gridgen, multigpu
+    s, _, _ = gridgen.make_config("c5_50", shape=(48, 64), seed=4)
+    cost = lambda b: max(multigpu.share_cost(int((s[b[i]:b[i + 1]] > 0.5).sum()), b[i + 1] - b[i])
+                         for i in range(len(b) - 1))
+    for world in (2, 4):
+        ov = multigpu.overlap_bounds(s, 0.5, world)
+        lin = P.plan_partition(s, 0.5, world, *multigpu.partition_weights())
+        assert ov[0] == 0 and ov[-1] == s.size and np.all(np.diff(ov) >= 0)
+        assert cost(ov) <= cost(lin) + 1e-12
