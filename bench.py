@@ -320,7 +320,7 @@ def run_gpu_arm(args):
         dist.barrier()
     ms_local = ev0.elapsed_time(ev1)
     ctx.check(stream)
-    if os.environ.get("BENCH_DEBUG"):
+    if os.environ.get("BENCH_DEBUG"):   # diagnostic: three more timed passes to stderr (run-to-run spread)
         print(f"debug: lo={lo} hi={hi} n={n} ms/step={ms_local / K:.4f}", file=sys.stderr)
         for rep in range(3):
             ev0.record(stream)
