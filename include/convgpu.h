@@ -118,6 +118,12 @@ typedef struct cvg_stats {
   double device_ms;          /* device time of the compute (CUDA events)      */
   double h2d_ms, d2h_ms;     /* staging copies (host buffers only)           */
   long long h2d_bytes, d2h_bytes;
+  long long n_recomputed;    /* deep levels whose relaxed stop decision fell
+                                in the guard band around newton_tol and were
+                                re-derived on the exact path (reference
+                                rounding, libm-exact exp)                     */
+  long long n_corrected;     /* columns that re-derivation rewrote (an update
+                                count differed from the relaxed one)          */
 } cvg_stats;
 
 typedef struct cvg_context cvg_context;
@@ -169,6 +175,11 @@ cvg_status cvg_ientropy_solve(cvg_context* ctx, long long n, const double* y,
 /* Device evaluation of approx_exp (physics.hpp:83) over n host values. */
 cvg_status cvg_approx_exp(cvg_context* ctx, long long n, const double* x,
                           double* out);
+
+/* Device evaluation of the Exact variant's exp_eval (physics.cpp:35: the
+ * libm exp) over n host values: bit-identical to glibc 2.39's exp (the
+ * restated algorithm of colmath.cuh exp_gl). */
+cvg_status cvg_exp(cvg_context* ctx, long long n, const double* x, double* out);
 
 /* --- Feedback loop (validate.cpp:113-206) ------------------------------ */
 

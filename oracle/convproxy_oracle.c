@@ -80,6 +80,77 @@ double orc_approx_exp(double x) {
   return ldexp(p, k);
 }
 
+/* The libm exp the reference calls for Exact/StrengthReduced (physics.cpp:35;
+ * glibc 2.39, not vendored, reached through <cmath>), restated
+ * so the device can evaluate it bit for bit (colmath.cuh exp_gl).  glibc's
+ * published algorithm (sysdeps/ieee754/dbl-64/e_exp.c, table-driven, N = 128,
+ * degree-5 polynomial; its FMA build on x86-64 contracts the main path's
+ * multiply-adds):
+ *   k = round(x 128/ln2), r = x - k ln2/128 (two-part constant),
+ *   exp(x) = 2^(k/128) (1 + tail_j + r + r^2 (C2 + r C3) + r^4 (C4 + r C5)),
+ * with the scaled special case for |x| in [512, 1024) (contracted for k > 0,
+ * uncontracted in the subnormal branch -- as measured against the libm) and
+ * 1 + x for |x| < 2^-54.  The table comes from tools/gen_exp_table.py (own
+ * computation); tests/test_oracle.py pins this restatement against the
+ * running libm over millions of arguments. */
+#include <string.h>
+#include "../paper_1711_00289_b200/csrc/exp_gl_table.h"
+static const uint64_t kExpGlTab[256] = {CVG_EXP_GL_TABLE};
+static uint64_t dbits(double x) { uint64_t u; memcpy(&u, &x, 8); return u; }
+static double bitsd(uint64_t u) { double x; memcpy(&x, &u, 8); return x; }
+
+static double exp_gl_special(double tmp, uint64_t sbits, uint64_t ki) {
+  if ((ki & 0x80000000u) == 0) {      /* k > 0: scale's exponent overflowed */
+    const double scale = bitsd(sbits - (1009ull << 52));
+    return 0x1p1009 * fma(scale, tmp, scale);
+  }
+  const double scale = bitsd(sbits + (1022ull << 52));  /* k < 0: subnormal range */
+  const double st = scale * tmp;
+  double y = scale + st;
+  if (y < 1.0) {
+    double lo = (scale - y) + st;
+    const double hi = 1.0 + y;
+    lo = ((1.0 - hi) + y) + lo;
+    y = (hi + lo) - 1.0;
+    if (y == 0.0) y = 0.0;
+  }
+  return 0x1p-1022 * y;
+}
+
+double orc_exp_gl(double x) {
+  uint32_t abstop = (uint32_t)(dbits(x) >> 52) & 0x7ff;
+  if (abstop - 0x3c9u >= 0x408u - 0x3c9u) {          /* |x| < 2^-54 or >= 512 */
+    if (abstop - 0x3c9u >= 0x80000000u) return 1.0 + x;
+    if (abstop >= 0x409u) {                           /* |x| >= 1024, inf, nan */
+      if (dbits(x) == dbits(-INFINITY)) return 0.0;
+      if (abstop >= 0x7ffu) return 1.0 + x;
+      return (dbits(x) >> 63) ? 0.0 : INFINITY;
+    }
+    abstop = 0;
+  }
+  double kd = fma(0x1.71547652b82fep7, x, 0x1.8p52);
+  const uint64_t ki = dbits(kd);
+  kd -= 0x1.8p52;
+  const double r = fma(kd, -0x1.cf79abc9e3b3ap-47, fma(kd, -0x1.62e42fefa0000p-8, x));
+  const uint64_t idx = 2 * (ki % 128);
+  const double tail = bitsd(kExpGlTab[idx]);
+  const uint64_t sbits = kExpGlTab[idx + 1] + (ki << 45);
+  const double r2 = r * r;
+  const double tmp = fma(r2 * r2, fma(r, 0x1.1111167a4d017p-7, 0x1.55555cf172b91p-5),
+                         fma(r2, fma(r, 0x1.555555555543cp-3, 0x1.ffffffffffdbdp-2), tail + r));
+  if (abstop == 0) return exp_gl_special(tmp, sbits, ki);
+  const double scale = bitsd(sbits);
+  return fma(scale, tmp, scale);
+}
+
+/* Vector forms for the pinning test: the restatement and the running libm. */
+void orc_exp_gl_vec(long long n, const double* x, double* out) {
+  for (long long i = 0; i < n; ++i) out[i] = orc_exp_gl(x[i]);
+}
+void orc_libm_exp_vec(long long n, const double* x, double* out) {
+  for (long long i = 0; i < n; ++i) out[i] = exp(x[i]);
+}
+
 /* physics.cpp:34-36 */
 static double exp_eval(double x, int variant) {
   return variant == ORC_APPROX_TRANSCENDENTAL ? orc_approx_exp(x) : exp(x);

@@ -48,6 +48,12 @@ double orc_rng_u01(uint64_t seed, uint64_t stream, uint64_t counter);
 /* physics.cpp:40-60 */
 double orc_approx_exp(double x);
 
+/* glibc 2.39 exp restated (the libm exp of physics.cpp:35); vector forms of
+ * it and of the running libm exp, for the pinning test. */
+double orc_exp_gl(double x);
+void orc_exp_gl_vec(long long n, const double* x, double* out);
+void orc_libm_exp_vec(long long n, const double* x, double* out);
+
 /* physics.cpp:64-87, :101-104.  Returns ORC_OK or a failure kind.
  * min_margin (nullable) receives min over convergence tests of
  * | |resid| - tol | / tol (the Newton-margin classifier). */

@@ -79,7 +79,8 @@ class Stats(C.Structure):
     _fields_ = [("n_columns", C.c_longlong), ("n_triggered", C.c_longlong),
                 ("failing_column", C.c_longlong), ("failure_kind", C.c_int),
                 ("failing_kernel", C.c_int), ("device_ms", C.c_double), ("h2d_ms", C.c_double),
-                ("d2h_ms", C.c_double), ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong)]
+                ("d2h_ms", C.c_double), ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong),
+                ("n_recomputed", C.c_longlong), ("n_corrected", C.c_longlong)]
 
 
 CVG_OK, CVG_ERR_INVALID, CVG_ERR_NUMERIC, CVG_ERR_CHECK, CVG_ERR_DEVICE = 0, 1, 3, 4, 6
@@ -156,6 +157,9 @@ def load_library():
     L.cvg_shallow_convection.argtypes = L.cvg_deep_convection.argtypes
     L.cvg_ientropy_solve.argtypes = [vp, i64, vp, vp, C.POINTER(KernelOptions), vp, vp]
     L.cvg_approx_exp.argtypes = [vp, i64, vp, vp]
+    if hasattr(L, "cvg_exp"):   # (absent only in pre-0.3 builds used for A/B timing)
+        L.cvg_exp.argtypes = [vp, i64, vp, vp]
+        L.cvg_exp.restype = C.c_int
     L.cvg_plan_partition.argtypes = [i64, vp, dbl, i32, dbl, dbl, vp]
     L.cvg_profile_begin.argtypes = [vp, i32]
     L.cvg_profile_end.argtypes = [vp, C.POINTER(C.c_int), vp, i32]
@@ -290,6 +294,14 @@ class Context:
         x = np.ascontiguousarray(np.atleast_1d(x), dtype=np.float64)
         out = np.empty_like(x)
         _raise(load_library().cvg_approx_exp(self._h, x.size, x.ctypes.data, out.ctypes.data))
+        return out
+
+    def exp(self, x):
+        """The Exact variant's exp_eval (physics.cpp:35) on the device:
+        bit-identical to the libm exp the reference calls."""
+        x = np.ascontiguousarray(np.atleast_1d(x), dtype=np.float64)
+        out = np.empty_like(x)
+        _raise(load_library().cvg_exp(self._h, x.size, x.ctypes.data, out.ctypes.data))
         return out
 
     # -- feedback loop (validate.cpp:113-206) ---------------------------------

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = [os.path.join(PKG, "csrc", "convgpu.cu")]
-DEPS = SOURCES + [os.path.join(PKG, "csrc", f) for f in ("colmath.cuh", "convgpu_kernels.cuh", "bulkcopy.cuh")] + [
+DEPS = SOURCES + [os.path.join(PKG, "csrc", f) for f in ("colmath.cuh", "convgpu_kernels.cuh", "bulkcopy.cuh", "exp_gl_table.h")] + [
     os.path.join(ROOT, "include", "convgpu.h")]
 
 

@@ -63,17 +63,14 @@ struct DevBuf {
   }
 };
 
-// 2^(j/512) as double-double (hi, lo), from x87 extended precision:
-// exp2l is accurate to ~1 ulp of the 64-bit significand, so hi + lo carries
-// ~2^-64 relative error -- far below the final double rounding.
-std::vector<double2> exp_table_host() {
-  std::vector<double2> t(cvg::kExpTableSize);
-  for (int j = 0; j < cvg::kExpTableSize; ++j) {
-    const long double v = exp2l(static_cast<long double>(j) / cvg::kExpTableSize);
-    const double hi = static_cast<double>(v);
-    const double lo = static_cast<double>(v - static_cast<long double>(hi));
-    t[j] = make_double2(hi, lo);
-  }
+// 2^(j/512) rounded to double for the relaxed Newton loop's exp (colmath.cuh
+// exp_fetch1), from x87 extended precision (~1 ulp of the 64-bit
+// significand, so the rounding to double is correct except in double-
+// rounding ties -- immaterial for a path whose stop decisions are guarded).
+std::vector<double> exp_table1_host() {
+  std::vector<double> t(cvg::kExpTableSize);
+  for (int j = 0; j < cvg::kExpTableSize; ++j)
+    t[j] = static_cast<double>(exp2l(static_cast<long double>(j) / cvg::kExpTableSize));
   return t;
 }
 
@@ -101,7 +98,9 @@ struct Workspace {
   cudaStream_t side = nullptr;    // shallow kernel, concurrent with deep
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf<long long> groups;            // compacted column groups with a triggered column
-  DevBuf<int> counters;                // [0] listed groups, [1] triggered columns
+  DevBuf<int> counters;                // [0] listed groups, [1] triggered columns, [2] levels queued
+                                       // for exact re-derivation, [3] columns rewritten by it
+  DevBuf<unsigned long long> redo;     // the redo list (guard band, redo_kernel)
   DevBuf<unsigned long long> cursor;   // [0] deep work cursor, [1..32] dummies
   DevBuf<unsigned long long> err;      // [0] deep, [1] shallow failure key
   unsigned long long* h_err = nullptr; // pinned mirror of err[0..1]
@@ -128,7 +127,7 @@ struct Workspace {
   void destroy() {
     for (auto* b : {&in_s, &in_T, &in_q, &dT, &dq, &dp, &sT, &sq, &sp}) b->release();
     dw.release(); sw.release(); dx.release(); sx.release();
-    groups.release(); counters.release(); cursor.release(); err.release();
+    groups.release(); counters.release(); cursor.release(); err.release(); redo.release();
     if (h_err) cudaFreeHost(h_err);
     if (h_count) cudaFreeHost(h_count);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -170,7 +169,8 @@ struct cvg_context {
   int num_sms = 0;
   cudaStream_t stream = nullptr;  // default stream of the async API
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_h0 = nullptr, ev_h1 = nullptr;
-  DevBuf<double2> exp_tab;
+  DevBuf<double> exp_tab1;              // relaxed loop's 2^(j/512) table
+  const double2* gl_tab = nullptr;       // exp_gl table (cvg::kExpGlTable, device symbol)
   Workspace ws[kSlots];
   DevBuf<double> aux0, aux1;
   DevBuf<int> auxi;
@@ -190,6 +190,13 @@ struct cvg_context {
   // without the occasional serialised schedule (0.70 ms) of mixed settings.
   int carveout = 72;
   bool far32 = true;       // CVG_FAR32: FP32 far phase of the relaxed Newton solve
+  // CVG_GUARD: relative half-width g of the guard band [tol (1-g), tol (1+g)]
+  // around newton_tol inside which a relaxed solve's stop decision is
+  // re-derived on the exact path (colmath.cuh); 0 disables the re-runs
+  // (then work_units may flip where the reference's residual is within
+  // rounding noise of tol)
+  double guard = 1.0 / 128;
+  bool redo_launch = true;  // CVG_REDO=0: skip the re-derivation kernels (timing experiments only)
   long long chunk_cols = kChunkCols;  // CVG_CHUNK_COLS: host-call pipeline chunk
   int slots = 3;                      // CVG_SLOTS: workspaces used by host-buffer calls (1..kSlots)
   const char* trace_path = nullptr;   // CVG_TRACE: per-block (kernel, smid, start, end)
@@ -271,9 +278,7 @@ static bool aligned32(const void* p) { return ((uintptr_t)p & 31) == 0; }
 template <int VAR, bool NARROW, int NW>
 void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
   const int threads = NW * 32;
-  const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
-                      (size_t)cvg::kExpTableSize * cvg::kTab1Copies * sizeof(double) +
-                      (size_t)NW * cvg::deep_warp_doubles(NARROW, a.L) * sizeof(double);
+  const size_t smem = cvg::deep_table_bytes() + (size_t)NW * cvg::deep_warp_doubles(NARROW, a.L) * sizeof(double);
   auto kern = cvg::deep_kernel<VAR, NARROW, NW>;
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
@@ -308,8 +313,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   const bool tpc = !lpc && dp && a.L <= 32 &&
                    (tpc_forced || (ctx->deep_tpc == 2 && a.n >= cvg::kTpcMinColumns));
   if (tpc || lpc) {
-    const size_t smem = (size_t)cvg::kExpTableSize * cvg::kTabCopies * sizeof(double2) +
-                        (size_t)cvg::kExpTableSize * cvg::kTab1Copies * sizeof(double);
+    const size_t smem = cvg::deep_table_bytes();
     // beside the shallow kernel: one 12-warp block per SM (registers capped
     // so three shallow blocks fit); alone: two 10-warp blocks per SM
     void (*kern)(cvg::DeepArgs) = nullptr;
@@ -344,6 +348,14 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
       if (nw == 16) launch_deep_t<VAR, false, 16>(ctx, a, st);
       else launch_deep_t<VAR, false, 12>(ctx, a, st);
     }
+  }
+  if (dp && a.relaxed && VAR != cvg::kVarApprox && ctx->guard > 0.0 && ctx->redo_launch) {
+    // exact re-derivation of the levels the guard band queued (usually a
+    // few microseconds, beside the shallow kernel's tail)
+    const size_t smem = (size_t)(cvg::kRedoThreads / 32) * a.L * sizeof(double);
+    cvg::redo_kernel<VAR><<<ctx->num_sms * 4, cvg::kRedoThreads, 0, st>>>(a);
+    cvg::fix_kernel<VAR><<<ctx->num_sms * 4, cvg::kRedoThreads, smem, st>>>(a);
+    CVG_CUDA(cudaGetLastError());
   }
   if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
   if (ov) {
@@ -414,6 +426,17 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.groups = w.groups.p; a.count = w.counters.p; a.cursor = w.cursor.p; a.n = n;
     a.err = w.err.p; a.first_col = in->first_col;
     a.thr = o->activity_threshold; a.tol = o->newton_tol; a.maxit = o->newton_max_iter;
+    a.tol_lo = o->newton_tol * (1.0 - ctx->guard);
+    a.tol_hi = o->newton_tol * (1.0 + ctx->guard);
+    // redo list: n/2 + 4096 entries (the f02 grid queues ~1.4 % of its
+    // triggered columns' levels at the default guard; beyond the capacity
+    // redo_kernel recomputes every triggered column exactly)
+    const long long cap = std::min<long long>(n / 2 + 4096, 0x3fffffffLL);
+    w.redo.ensure(2 * (size_t)cap);   // [cap] queued levels, [cap] columns to rewrite
+    a.redo = w.redo.p;
+    a.redo_cap = (int)cap;
+    a.redo_count = w.counters.p + 2;
+    a.fix_count = w.counters.p + 3;
     a.L = L;
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
     a.relaxed = !strict;
@@ -422,7 +445,8 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.tree_precip = !strict && o->variant != CVG_APPROX_TRANSCENDENTAL && o->newton_tol >= 0x1.0p-40;
     a.vec4 = deep->ld % 4 == 0 && aligned32(deep->tend_T) && aligned32(deep->tend_q);
   }
-  a.exp_tab = ctx->exp_tab.p;
+  a.gl_tab = ctx->gl_tab;
+  a.exp_tab1 = ctx->exp_tab1.p;
   if (pe) CVG_CUDA(cudaEventRecord(pe[1], st));
   cvg::ShallowArgs b{};
   b.s = in->s; b.T = in->T; b.q = in->q; b.ld_in = in->ld; b.n = n;
@@ -434,7 +458,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     b.d_tend_T = deep->tend_T; b.d_tend_q = deep->tend_q; b.d_precip = deep->precip;
     b.d_work = deep->work_units; b.d_exited = deep->exited_early; b.d_ld_out = deep->ld;
   }
-  b.err = w.err.p + 1; b.exp_tab = ctx->exp_tab.p; b.first_col = in->first_col;
+  b.err = w.err.p + 1; b.gl_tab = ctx->gl_tab; b.first_col = in->first_col;
   b.thr = o->activity_threshold; b.L = L;
   if (ctx->trace_path && &w == &ctx->ws[0]) {
     ctx->trace_d.ensure(3 * 4096);
@@ -454,17 +478,20 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
 // Queues the D2H of a workspace's latched failure words / trigger count.
 void read_flags_async(Workspace& w, cudaStream_t st) {
   CVG_CUDA(cudaMemcpyAsync(w.h_err, w.err.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  CVG_CUDA(cudaMemcpyAsync(w.h_count, w.counters.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CVG_CUDA(cudaMemcpyAsync(w.h_count, w.counters.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
 }
 
 // Turns the folded failure keys (minimum over the call's chunks) into the
 // reference's error: deep first, then shallow, as the reference runs
 // deep_convection then shallow_convection; the lowest failing column.
 cvg_status collect(const unsigned long long* keys_deep, const unsigned long long* keys_sh, long long triggered,
-                   int mask, int maxit, long long n, cvg_stats* stats) {
+                   long long recomputed, long long corrected, int mask, int maxit, long long n,
+                   cvg_stats* stats) {
   if (stats) {
     stats->n_columns = n;
     stats->n_triggered = (mask & CVG_DEEP) ? triggered : 0;
+    stats->n_recomputed = (mask & CVG_DEEP) ? recomputed : 0;
+    stats->n_corrected = (mask & CVG_DEEP) ? corrected : 0;
     stats->failing_column = -1;
     stats->failure_kind = 0;
     stats->failing_kernel = 0;
@@ -535,7 +562,7 @@ constexpr long long pitch_cols(long long m) { return (m + 31) & ~31LL; }
 
 extern "C" {
 
-const char* cvg_version(void) { return "0.2.0"; }
+const char* cvg_version(void) { return "0.3.0"; }
 
 const char* cvg_last_error(void) { return g_last_error.c_str(); }
 
@@ -576,6 +603,8 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_RESET_KERNEL")) ctx->reset_kernel = atoi(e) != 0;
     if (const char* e = getenv("CVG_CARVEOUT")) ctx->carveout = atoi(e);
     if (const char* e = getenv("CVG_FAR32")) ctx->far32 = atoi(e) != 0;
+    if (const char* e = getenv("CVG_GUARD")) ctx->guard = std::max(0.0, std::min(0.5, atof(e)));
+    if (const char* e = getenv("CVG_REDO")) ctx->redo_launch = atoi(e) != 0;
     if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
     if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
@@ -584,9 +613,12 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     try {
       CVG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
       for (cudaEvent_t* e : {&ctx->ev0, &ctx->ev1, &ctx->ev_h0, &ctx->ev_h1}) CVG_CUDA(cudaEventCreate(e));
-      const std::vector<double2> tab = exp_table_host();
-      ctx->exp_tab.ensure(tab.size());
-      CVG_CUDA(cudaMemcpy(ctx->exp_tab.p, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
+      const std::vector<double> tab = exp_table1_host();
+      ctx->exp_tab1.ensure(tab.size());
+      CVG_CUDA(cudaMemcpy(ctx->exp_tab1.p, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+      void* gl = nullptr;
+      CVG_CUDA(cudaGetSymbolAddress(&gl, cvg::kExpGlTable));
+      ctx->gl_tab = static_cast<const double2*>(gl);
       for (Workspace& w : ctx->ws) w.create();
       ctx->aux_err.ensure(1);
       CVG_CUDA(cudaMallocHost(&ctx->h_aux_err, sizeof(unsigned long long)));
@@ -603,7 +635,7 @@ void cvg_context_free(cvg_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
-  ctx->exp_tab.release();
+  ctx->exp_tab1.release();
   for (Workspace& w : ctx->ws) w.destroy();
   ctx->aux0.release();
   ctx->aux1.release();
@@ -738,7 +770,8 @@ cvg_status cvg_convect_check(cvg_context* ctx, void* stream, cvg_stats* stats) {
         fclose(f);
       }
     }
-    return collect(&w.h_err[0], &w.h_err[1], w.h_count[1], ctx->last_mask, ctx->last_maxit, ctx->last_n, stats);
+    return collect(&w.h_err[0], &w.h_err[1], w.h_count[1], w.h_count[2], w.h_count[3], ctx->last_mask,
+                   ctx->last_maxit, ctx->last_n, stats);
   });
 }
 
@@ -782,13 +815,15 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
     long long h2d = 0, d2h = 0;
     CVG_CUDA(cudaEventRecord(ctx->ev_h0, ctx->stream));
     unsigned long long md = ~0ULL, ms_ = ~0ULL;
-    long long trig = 0;
+    long long trig = 0, recomp = 0, corr = 0;
     bool busy[kSlots] = {};
     auto drain = [&](Workspace& w) {  // a slot's previous chunk: wait, fold its flags
       CVG_CUDA(cudaStreamSynchronize(w.stream));
       md = std::min(md, w.h_err[0]);
       ms_ = std::min(ms_, w.h_err[1]);
       trig += w.h_count[1];
+      recomp += w.h_count[2];
+      corr += w.h_count[3];
     };
     for (long long ci = 0; ci < nchunks; ++ci) {
       const int slot = (int)(ci % ctx->slots);
@@ -848,7 +883,7 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
     }
     for (int s = 0; s < kSlots; ++s)
       if (busy[s]) drain(ctx->ws[s]);
-    cvg_status rc = collect(&md, &ms_, trig, mask, opts->newton_max_iter, n, stats);
+    cvg_status rc = collect(&md, &ms_, trig, recomp, corr, mask, opts->newton_max_iter, n, stats);
     if (stats) {
       for (int s = 0; s < kSlots; ++s) {
         CVG_CUDA(cudaEventRecord(ctx->ev1, ctx->ws[s].stream));
@@ -900,9 +935,9 @@ cvg_status cvg_ientropy_solve(cvg_context* ctx, long long n, const double* y, co
     const unsigned blocks = (unsigned)((n + 255) / 256);
     switch (opts->variant) {
       case 2: cvg::ientropy_kernel<cvg::kVarApprox><<<blocks, 256, 0, st>>>(dy, dg, n, opts->newton_tol,
-                  opts->newton_max_iter, ctx->aux0.p, ctx->auxi.p, ctx->aux_err.p, ctx->exp_tab.p); break;
+                  opts->newton_max_iter, ctx->aux0.p, ctx->auxi.p, ctx->aux_err.p, ctx->gl_tab); break;
       default: cvg::ientropy_kernel<cvg::kVarExact><<<blocks, 256, 0, st>>>(dy, dg, n, opts->newton_tol,
-                  opts->newton_max_iter, ctx->aux0.p, ctx->auxi.p, ctx->aux_err.p, ctx->exp_tab.p); break;
+                  opts->newton_max_iter, ctx->aux0.p, ctx->auxi.p, ctx->aux_err.p, ctx->gl_tab); break;
     }
     CVG_CUDA(cudaGetLastError());
     CVG_CUDA(cudaMemcpyAsync(root, ctx->aux0.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
@@ -930,6 +965,24 @@ cvg_status cvg_approx_exp(cvg_context* ctx, long long n, const double* x, double
     ctx->aux1.ensure(n);
     CVG_CUDA(cudaMemcpyAsync(ctx->aux1.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     cvg::approx_exp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ctx->aux1.p, ctx->aux0.p, n);
+    CVG_CUDA(cudaGetLastError());
+    CVG_CUDA(cudaMemcpyAsync(out, ctx->aux0.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CVG_CUDA(cudaStreamSynchronize(st));
+    return CVG_OK;
+  });
+}
+
+cvg_status cvg_exp(cvg_context* ctx, long long n, const double* x, double* out) {
+  if (!ctx || (n > 0 && (!x || !out))) return fail(CVG_ERR_INVALID, "cvg_exp: null argument");
+  if (n < 0) return fail(CVG_ERR_INVALID, "cvg_exp: n < 0");
+  return guarded([&] {
+    if (n == 0) return CVG_OK;
+    CVG_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    ctx->aux0.ensure(n);
+    ctx->aux1.ensure(n);
+    CVG_CUDA(cudaMemcpyAsync(ctx->aux1.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    cvg::exp_gl_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ctx->aux1.p, ctx->aux0.p, n, ctx->gl_tab);
     CVG_CUDA(cudaGetLastError());
     CVG_CUDA(cudaMemcpyAsync(out, ctx->aux0.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     CVG_CUDA(cudaStreamSynchronize(st));
@@ -1046,7 +1099,7 @@ void leg_step(cvg_context* ctx, const cvg_options* o, int kernel, long long n, i
 cvg_status leg_errors(const unsigned long long* h_err, int nlegs, int kernel, int maxit, long long n) {
   for (int l = 0; l < nlegs; ++l) {
     const unsigned long long* e = h_err + 2 * l;
-    if (e[0] != ~0ULL || e[1] != ~0ULL) return collect(&e[0], &e[1], 0, kernel, maxit, n, nullptr);
+    if (e[0] != ~0ULL || e[1] != ~0ULL) return collect(&e[0], &e[1], 0, 0, 0, kernel, maxit, n, nullptr);
   }
   return CVG_OK;
 }

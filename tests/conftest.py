@@ -45,3 +45,19 @@ def env_context(**env):
                 del os.environ[k]
             else:
                 os.environ[k] = v
+
+
+def exp_arguments(n=1_000_000, seed=3):
+    """Arguments for the exp pinning tests: the Newton range of the deep
+    solves (x = 0.05 t, t from the guesses down to far-left roots), the
+    shallow exp(-50 q) range, the scaled special cases |x| in [512, 1024),
+    tiny |x| < 2^-54, non-finite values and random bit patterns."""
+    import numpy as np
+    r = np.random.default_rng(seed)
+    t = r.uniform(-6100.0, 1300.0, n)
+    parts = [0.05 * t, r.uniform(-760.0, 720.0, n // 2), -50.0 * r.uniform(0.0, 0.03, n // 4),
+             r.uniform(-1.0, 1.0, n // 8) * 2.0 ** -r.integers(40, 80, n // 8),
+             r.integers(0, 2 ** 63, n // 8, dtype=np.int64).view(np.float64),
+             np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 709.78, 709.79, -708.4, -745.1, -745.2, 512.0,
+                       -512.0, 1024.0, -1024.0, 2.0 ** -54, -(2.0 ** -54), 2.0 ** -55])]
+    return np.concatenate(parts)

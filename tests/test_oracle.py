@@ -252,3 +252,16 @@ def test_reference_packed_bytes_formula(nd):
     L = 30
     assert O.ref_packed_bytes(nd, L, True) == (8 * nd * (2 * L + 1) + 32, 16 * nd * L + 17 * nd)
     assert O.ref_packed_bytes(nd, L, False) == (8 * nd * (2 * L + 1), 16 * nd * L + 17 * nd)
+
+
+def test_exp_restatement_bit_exact_against_libm():
+    """orc_exp_gl (glibc 2.39's table-driven exp restated, with the table from
+    tools/gen_exp_table.py) equals the running libm exp -- the exp the
+    reference calls for Exact/StrengthReduced (physics.cpp:35) -- bit for bit.
+    The device's exp_gl (colmath.cuh) is the same restatement; with it the
+    strict Newton path reproduces the reference's iterates exactly."""
+    from conftest import exp_arguments
+    x = exp_arguments()
+    a, b = O.exp_gl(x), O.libm_exp(x)
+    same = (a.view(np.int64) == b.view(np.int64)) | (np.isnan(a) & np.isnan(b))
+    assert same.all(), f"{int((~same).sum())} of {x.size} differ, e.g. x={x[~same][:4]}"

@@ -2,18 +2,17 @@
 same seeded inputs -- all five BASELINE configs x all three variants -- and
 against the golden fixtures the reference itself produced.
 
-Parity rule (BASELINE.json north_star), written here:
+Parity rule (BASELINE.json north_star), written here and
+applied to EVERY column with no Newton-margin exemption:
   * deep trigger flags and shallow exit flags: exact (shallow flags exempt
-    where the exit predicate is within 1e-9 relative of its theta);
-  * work_units: exact, except deep columns whose Newton residual came within
-    1e-3 relative of newton_tol (the glibc-vs-device exp classifier); for the
-    ApproxTranscendental variant exact everywhere (pure IEEE arithmetic);
-  * fp64 fields: within 1e-10 relative or 1e-14 absolute, every column --
-    except that in a deep column whose work_units flipped inside the margin
-    class the absolute bound is 1e-12: one Newton update more or less moves
-    that solve's root by |resid| / f' <= 1e-12 / 0.07, which shifts tend_T by
-    0.04 dr and precip by q dr (measured worst: 2.4e-13 on a precip of 1e-4,
-    full c5_95 grid, column 644381, with or without the FP32 far phase).
+    where the exit predicate is within 1e-9 relative of its theta -- the
+    north star's near-threshold rule; no column of any grid falls there);
+  * work_units: exact, every variant, every device path.  The device's exp
+    is the libm's bit for bit (colmath.cuh exp_gl), so the strict path runs
+    the reference's own iterates; the default relaxed path re-runs exactly
+    any solve whose stop decision falls in the guard band around newton_tol
+    (colmath.cuh), so its counts are the reference's too;
+  * fp64 fields: within 1e-10 relative or 1e-14 absolute.
 """
 import glob
 import os
@@ -28,34 +27,24 @@ from paper_1711_00289_b200 import gridgen as G
 pytestmark = pytest.mark.gpu
 
 REL, ABS = 1e-10, 1e-14
-ABS_FLIPPED = 1e-12
-NEWTON_MARGIN = 1e-3
 PRED_MARGIN = 1e-9
 GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
 
 
-def check(got: P.ColumnOutputs, want, kernel: str, margin=None, bitexact_work=False):
-    """want: oracle Result or dict of golden arrays."""
+def check(got: P.ColumnOutputs, want, kernel: str, margin=None):
+    """want: oracle Result or dict of golden arrays.  Returns the number of
+    work_units mismatches (always 0 when it returns)."""
     g = (lambda f: getattr(want, f)) if not isinstance(want, dict) else (lambda f: want[f])
     margin = g("margin") if margin is None and not isinstance(want, dict) else margin
     exempt = np.zeros(got.exited_early.shape, bool)
     if kernel == "shallow" and margin is not None:
         exempt = margin < PRED_MARGIN
     assert np.array_equal(got.exited_early[~exempt], g("exited")[~exempt]), f"{kernel}: exit/trigger flags differ"
-    flip = got.work_units != g("work")
-    abs_col = np.full(flip.shape, ABS)
-    if kernel == "deep" and margin is not None and not bitexact_work:
-        abs_col[flip & (margin < NEWTON_MARGIN)] = ABS_FLIPPED
-    if bitexact_work:
-        assert not flip.any(), f"{kernel}: work_units differ in {int(flip.sum())} columns"
-    elif kernel == "deep" and margin is not None:
-        bad = flip & (margin >= NEWTON_MARGIN)
-        assert not bad.any(), f"deep: work_units differ outside the Newton-margin class: {np.nonzero(bad)[0][:8]}"
-    elif kernel == "shallow":
-        assert not (flip & ~exempt).any(), "shallow: phase counts differ"
+    flip = (got.work_units != g("work")) & ~exempt
+    assert not flip.any(), f"{kernel}: work_units differ in {int(flip.sum())} columns: {np.nonzero(flip)[0][:8]}"
     for f in ("tend_T", "tend_q", "precip"):
         a, b = getattr(got, f), g(f)
-        ok = np.abs(a - b) <= np.maximum(REL * np.abs(b), abs_col)
+        ok = np.abs(a - b) <= np.maximum(REL * np.abs(b), ABS)
         assert ok.all(), f"{kernel}.{f}: {int((~ok).sum())} values outside tolerance, max |d| {np.max(np.abs(a - b))}"
     return int(flip.sum())
 
@@ -73,8 +62,8 @@ def test_convect_matches_oracle(ctx, cfg, kw, variant):
     deep, sh = ctx.convect(s, T, q, P.KernelOptions(variant=variant, activity_threshold=thr))
     oo = O.Options(variant=variant, activity_threshold=thr)
     od, osh = O.convection("deep", s, T, q, oo), O.convection("shallow", s, T, q, oo)
-    check(deep, od, "deep", bitexact_work=(variant == 2))
-    check(sh, osh, "shallow", bitexact_work=(variant == 2))
+    check(deep, od, "deep")
+    check(sh, osh, "shallow")
     assert ctx.last_stats.n_triggered == int((od.exited == 0).sum())
 
 
@@ -89,7 +78,7 @@ def test_convect_matches_reference_golden(ctx, path):
         sm = O.convection("shallow", g["s"], g["T"], g["q"], oo).margin
         for k, got, m in (("deep", deep, dm), ("shallow", sh, sm)):
             want = {f: g[f"{k}_v{v}_{f}"] for f in ("tend_T", "tend_q", "precip", "work", "exited")}
-            check(got, want, k, margin=m, bitexact_work=(v == 2))
+            check(got, want, k, margin=m)
 
 
 def test_approx_variant_roots_bit_exact(ctx):
@@ -116,9 +105,8 @@ def test_full_size_strided_parity(ctx, cfg):
     osh = O.convection("shallow", sub(s), sub(T), sub(q))
     pick = lambda o: P.ColumnOutputs(o.tend_T[:, idx], o.tend_q[:, idx], o.precip[idx], o.work_units[idx],
                                      o.exited_early[idx])
-    flips = check(pick(deep), od, "deep")
+    check(pick(deep), od, "deep")
     check(pick(sh), osh, "shallow")
-    assert flips <= 0.001 * idx.size
     # size-independent properties over the whole grid
     trig = deep.exited_early == 0
     assert trig.sum() == ctx.last_stats.n_triggered == int((s > 0.5).sum())
@@ -126,6 +114,26 @@ def test_full_size_strided_parity(ctx, cfg):
     assert ((deep.work_units[trig] >= 2 * 30) & (deep.work_units[trig] <= 2 * 30 * 100)).all()
     assert np.isin(sh.work_units, [30, 60, 90, 120]).all()
     assert not sh.tend_q[:, sh.exited_early == 1].any()
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_c3_full_size_every_column(ctx, variant):
+    """BASELINE config 3 at its stated size: the f09-shaped 192 x 288 grid
+    (55,296 columns) at activity_threshold 0.75 (30 % deep, 25 % shallow-only
+    survivors), every column against the oracle."""
+    s, T, q = G.make_config("c3", seed=42)
+    assert s.size == 55296
+    thr = G.config_threshold("c3")
+    assert thr == 0.75
+    deep, sh = ctx.convect(s, T, q, P.KernelOptions(variant=variant, activity_threshold=thr))
+    oo = O.Options(variant=variant, activity_threshold=thr)
+    od, osh = O.convection("deep", s, T, q, oo), O.convection("shallow", s, T, q, oo)
+    check(deep, od, "deep")
+    check(sh, osh, "shallow")
+    trig = s > thr
+    assert abs(trig.mean() - 0.30) < 0.01
+    surv_only = (~trig) & (osh.exited == 0)
+    assert abs(surv_only.mean() - 0.25) < 0.03
 
 
 def test_determinism(ctx):
@@ -153,6 +161,17 @@ def test_ientropy_batch_known_answers(ctx):
             assert st == 0 and abs(rr - r2) <= 1e-12 * max(1.0, abs(r2))
             if v == 2:
                 assert rr == r2 and ii == i2
+
+
+def test_exp_bit_exact_against_libm(ctx):
+    """The device exp_gl (colmath.cuh) equals the libm exp the reference calls
+    (physics.cpp:35) bit for bit: Newton range, shallow range, the scaled
+    special cases, tiny and non-finite arguments, random bit patterns."""
+    from conftest import exp_arguments
+    x = exp_arguments()
+    got, want = ctx.exp(x), O.libm_exp(x)
+    same = (got.view(np.int64) == want.view(np.int64)) | (np.isnan(got) & np.isnan(want))
+    assert same.all(), f"{int((~same).sum())} differ, e.g. x={x[~same][:4]}"
 
 
 def test_approx_exp_bit_exact(ctx):
@@ -187,12 +206,13 @@ def test_strict_update_matches_oracle_and_relaxed(ctx, strict_ctx, cfg, kw, vari
     check(s_strict, osh, "shallow")
     check(d_relax, od, "deep")
     check(s_relax, osh, "shallow")
-    # the two device paths differ only by rounding noise: same flags, work
-    # equal outside the Newton-margin class, fp64 fields within tolerance
-    check(d_relax, {"tend_T": d_strict.tend_T, "tend_q": d_strict.tend_q, "precip": d_strict.precip,
-                    "work": d_strict.work_units, "exited": d_strict.exited_early}, "deep", margin=od.margin)
+    # strict = the reference's own roundings with the libm's exp: the
+    # precipitation roots, their k-order sum and the counts are bit-identical
+    # (only tend_T / tend_q go through sin)
+    assert np.array_equal(d_strict.precip.view(np.int64), od.precip.view(np.int64))
+    assert np.array_equal(d_strict.work_units, od.work)
     # strict shallow keeps the reference's per-term phase sums: bit-identical
-    # flags and phase counts, fp64 fields equal to the oracle's roundings
+    # flags and phase counts
     assert np.array_equal(s_strict.work_units, osh.work) and np.array_equal(s_strict.exited_early, osh.exited)
 
 
@@ -211,13 +231,14 @@ def test_relaxed_guard_falls_back_for_tight_tolerance(ctx, strict_ctx):
 def test_far32_full_grid_every_column(ctx, cfg):
     """The FP32 far phase of the relaxed Newton solve (default for Exact;
     colmath.cuh newton_far32_step) against the oracle on EVERY column of the
-    full 884,736-column grid: flags exact, work_units exact outside the
-    Newton-margin class, fp64 fields within tolerance."""
+    full 884,736-column grid: flags and work_units exact (the guard band
+    re-runs the solves whose stop decision is within rounding noise of tol),
+    fp64 fields within tolerance."""
     s, T, q = G.make_config(cfg, seed=42)
     deep, sh = ctx.convect(s, T, q, P.KernelOptions())
+    assert ctx.last_stats.n_recomputed > 0   # the guard band did re-run solves
     od = O.convection("deep", s, T, q)
-    flips = check(deep, od, "deep")
-    assert flips <= 1e-3 * max(1, int((s > 0.5).sum()))   # 74 at c4 (all inside the margin class)
+    check(deep, od, "deep")
     check(sh, O.convection("shallow", s, T, q), "shallow")
 
 
@@ -225,8 +246,7 @@ def test_far32_full_grid_every_column(ctx, cfg):
 @pytest.mark.parametrize("cfg,kw", [("c2", {}), ("c3", {"shape": (96, 144)}), ("c5_95", {"shape": (64, 96)})],
                          ids=["c2", "c3", "c5_95"])
 def test_far32_against_fp64_update(ctx, cfg, kw, variant):
-    """far32 on vs off (CVG_FLAG_NO_FAR32): both match the oracle, and each
-    other up to rounding noise (work equal outside the margin class)."""
+    """far32 on vs off (CVG_FLAG_NO_FAR32): both match the oracle."""
     s, T, q = G.make_config(cfg, seed=21, **kw)
     thr = G.config_threshold(cfg)
     oo = O.Options(variant=variant, activity_threshold=thr)
@@ -235,8 +255,6 @@ def test_far32_against_fp64_update(ctx, cfg, kw, variant):
     b, _ = ctx.convect(s, T, q, P.KernelOptions(variant=variant, activity_threshold=thr, far32=False))
     check(a, od, "deep")
     check(b, od, "deep")
-    check(a, {"tend_T": b.tend_T, "tend_q": b.tend_q, "precip": b.precip, "work": b.work_units,
-              "exited": b.exited_early}, "deep", margin=od.margin)
 
 
 @pytest.mark.parametrize("tol", [1e-12, 1e-6, 2e-6, 2.0 ** -40, 1e-13])
@@ -277,8 +295,8 @@ def test_thread_per_column_kernel_matches_oracle(tpc_ctx, cfg, kw, variant):
     thr = G.config_threshold(cfg)
     deep, sh = tpc_ctx.convect(s, T, q, P.KernelOptions(variant=variant, activity_threshold=thr))
     oo = O.Options(variant=variant, activity_threshold=thr)
-    check(deep, O.convection("deep", s, T, q, oo), "deep", bitexact_work=(variant == 2))
-    check(sh, O.convection("shallow", s, T, q, oo), "shallow", bitexact_work=(variant == 2))
+    check(deep, O.convection("deep", s, T, q, oo), "deep")
+    check(sh, O.convection("shallow", s, T, q, oo), "shallow")
 
 
 @pytest.mark.parametrize("n", [1, 5, 31, 33, 1001])
@@ -310,8 +328,8 @@ def test_full_grid_variants_and_strict(ctx, variant, strict):
     od = O.convection("deep", sub(s), sub(T), sub(q), O.Options(variant=variant))
     pick = P.ColumnOutputs(deep.tend_T[:, idx], deep.tend_q[:, idx], deep.precip[idx], deep.work_units[idx],
                            deep.exited_early[idx])
-    check(pick, od, "deep", bitexact_work=(variant == 2))
-    if variant == 2:
+    check(pick, od, "deep")
+    if variant == 2 or strict:
         assert np.array_equal(pick.precip.view(np.int64), od.precip.view(np.int64))
 
 
