@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -55,6 +56,17 @@ struct DevBuf {
     cap = 0;
     CVG_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
     cap = n;
+  }
+  // Grows to n elements keeping the old allocation alive in `retired`
+  // (a CUDA graph captured earlier may still reference it); true if grown.
+  bool grow(size_t n, std::vector<void*>& retired) {
+    if (n <= cap) return false;
+    if (p) retired.push_back(p);
+    p = nullptr;
+    cap = 0;
+    CVG_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    cap = n;
+    return true;
   }
   void release() {
     if (p) cudaFree(p);
@@ -100,8 +112,9 @@ struct Workspace {
   DevBuf<long long> groups;            // compacted column groups with a triggered column
   DevBuf<int> counters;                // [0] listed groups, [1] triggered columns, [2] levels queued
                                        // for exact re-derivation, [3] columns rewritten by it
-  DevBuf<unsigned long long> redo;     // the redo list (guard band, redo_kernel)
-  DevBuf<unsigned long long> cursor;   // [0] deep work cursor, [1..32] dummies
+  DevBuf<unsigned long long> redo;     // the redo list (guard band): [cap][kRedoWords]
+  DevBuf<unsigned long long> fix;      // exact patches: [2 cap][3]
+  DevBuf<unsigned long long> cursor;   // [0] deep work cursor, [16] redo_kernel's finished blocks
   DevBuf<unsigned long long> err;      // [0] deep, [1] shallow failure key
   unsigned long long* h_err = nullptr; // pinned mirror of err[0..1]
   int* h_count = nullptr;              // pinned mirror of counters[0..1]
@@ -127,7 +140,7 @@ struct Workspace {
   void destroy() {
     for (auto* b : {&in_s, &in_T, &in_q, &dT, &dq, &dp, &sT, &sq, &sp}) b->release();
     dw.release(); sw.release(); dx.release(); sx.release();
-    groups.release(); counters.release(); cursor.release(); err.release(); redo.release();
+    groups.release(); counters.release(); cursor.release(); err.release(); redo.release(); fix.release();
     if (h_err) cudaFreeHost(h_err);
     if (h_count) cudaFreeHost(h_count);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -196,7 +209,7 @@ struct cvg_context {
   // (then work_units may flip where the reference's residual is within
   // rounding noise of tol)
   double guard = 1.0 / 128;
-  bool redo_launch = true;  // CVG_REDO=0: skip the re-derivation kernels (timing experiments only)
+  bool redo_launch = true;  // CVG_REDO=0: skip the re-derivation kernel (timing experiments only)
   long long chunk_cols = kChunkCols;  // CVG_CHUNK_COLS: host-call pipeline chunk
   int slots = 3;                      // CVG_SLOTS: workspaces used by host-buffer calls (1..kSlots)
   const char* trace_path = nullptr;   // CVG_TRACE: per-block (kernel, smid, start, end)
@@ -227,6 +240,7 @@ struct cvg_context {
   DevBuf<unsigned long long> loop_err;
   DevBuf<unsigned> loop_flag;
   bool reset_kernel = true;   // CVG_RESET_KERNEL: one reset launch instead of three memsets
+  std::vector<void*> retired;  // grown-out workspace buffers (graphs may reference them)
 };
 
 namespace {
@@ -349,12 +363,12 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
       else launch_deep_t<VAR, false, 12>(ctx, a, st);
     }
   }
-  if (dp && a.relaxed && VAR != cvg::kVarApprox && ctx->guard > 0.0 && ctx->redo_launch) {
-    // exact re-derivation of the levels the guard band queued (usually a
-    // few microseconds, beside the shallow kernel's tail)
-    const size_t smem = (size_t)(cvg::kRedoThreads / 32) * a.L * sizeof(double);
-    cvg::redo_kernel<VAR><<<ctx->num_sms * 4, cvg::kRedoThreads, 0, st>>>(a);
-    cvg::fix_kernel<VAR><<<ctx->num_sms * 4, cvg::kRedoThreads, smem, st>>>(a);
+  if (dp && a.relaxed && VAR != cvg::kVarApprox && ctx->redo_launch) {
+    // exact re-derivation of the solves the guard band flagged (a few
+    // microseconds: one exact solve per thread, patches by the last block)
+    const size_t smem = std::max((size_t)(cvg::kRedoThreads / 32) * a.L * sizeof(double),
+                                 (size_t)cvg::kFixStaged * sizeof(unsigned long long));
+    cvg::redo_kernel<VAR><<<ctx->num_sms * 2, cvg::kRedoThreads, smem, st>>>(a);
     CVG_CUDA(cudaGetLastError());
   }
   if (pe) CVG_CUDA(cudaEventRecord(pe[2], st));
@@ -392,6 +406,19 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   }
 }
 
+// Redo list capacity of an n-column call: n/2 + 4096 queued levels (the f02
+// grid queues ~1.4 % of its triggered columns' levels at the default guard;
+// beyond the capacity fix_kernel recomputes every triggered column exactly).
+long long redo_capacity(long long n) { return std::min<long long>(n / 2 + 4096, 0x3fffffffLL); }
+
+// Sizes workspace w for an n-column deep call.  Buffers only grow, and a
+// grown buffer's old allocation is retired (freed with the context), never
+// freed under a CUDA graph that may still use it.  Growth while `st` is
+// being captured (a caller's graph) is refused: allocation is not capturable
+// and the graph would bake in the size -- size the workspace with one
+// uncaptured call first.
+void prepare_ws(cvg_context* ctx, Workspace& w, long long n, cudaStream_t st);
+
 // Enqueues the hot path on `st` with workspace `w`: memsets of the per-call
 // cursors and failure words, the trigger + compaction kernel (deep
 // requested), then the deep and shallow kernels.  Pointers are device
@@ -401,21 +428,21 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
   const long long n = in->n_columns;
   const int L = in->n_levels;
   if (ctx->reset_kernel) {
-    cvg::reset_call_words_kernel<<<1, 32, 0, st>>>(w.counters.p, 4, w.cursor.p, 17, w.err.p, 2);
+    cvg::reset_call_words_kernel<<<1, 32, 0, st>>>(w.counters.p, 4, w.cursor.p, 20, w.err.p, 2);
     CVG_CUDA(cudaGetLastError());
   } else {
     CVG_CUDA(cudaMemsetAsync(w.counters.p, 0, 4 * sizeof(int), st));
-    CVG_CUDA(cudaMemsetAsync(w.cursor.p, 0, 17 * sizeof(unsigned long long), st));
+    CVG_CUDA(cudaMemsetAsync(w.cursor.p, 0, 20 * sizeof(unsigned long long), st));
     CVG_CUDA(cudaMemsetAsync(w.err.p, 0xff, 2 * sizeof(unsigned long long), st));
   }
   if (n == 0) return;
   const bool do_deep = (mask & CVG_DEEP) != 0, do_sh = (mask & CVG_SHALLOW) != 0;
   const bool strict = ctx->strict || (o->flags & CVG_FLAG_STRICT) != 0;
+  if (do_deep) prepare_ws(ctx, w, n, st);
   if (pe) CVG_CUDA(cudaEventRecord(pe[0], st));
   cvg::DeepArgs a{};
   if (do_deep) {
     const long long ngroups = (n + cvg::kGroupCols - 1) / cvg::kGroupCols;
-    w.groups.ensure((size_t)ngroups);
     const unsigned tb = (unsigned)((ngroups + cvg::kTrigThreads - 1) / cvg::kTrigThreads);
     cvg::trigger_groups_kernel<<<tb, cvg::kTrigThreads, 0, st>>>(in->s, n, o->activity_threshold, in->first_col,
                                                                   w.groups.p, w.counters.p, w.err.p);
@@ -428,21 +455,19 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.thr = o->activity_threshold; a.tol = o->newton_tol; a.maxit = o->newton_max_iter;
     a.tol_lo = o->newton_tol * (1.0 - ctx->guard);
     a.tol_hi = o->newton_tol * (1.0 + ctx->guard);
-    // redo list: n/2 + 4096 entries (the f02 grid queues ~1.4 % of its
-    // triggered columns' levels at the default guard; beyond the capacity
-    // redo_kernel recomputes every triggered column exactly)
-    const long long cap = std::min<long long>(n / 2 + 4096, 0x3fffffffLL);
-    w.redo.ensure(2 * (size_t)cap);   // [cap] queued levels, [cap] columns to rewrite
     a.redo = w.redo.p;
-    a.redo_cap = (int)cap;
+    a.fix = w.fix.p;
+    a.blocks_done = reinterpret_cast<unsigned*>(w.cursor.p + 16);   // reset per call
+    a.redo_cap = (int)redo_capacity(n);
     a.redo_count = w.counters.p + 2;
     a.fix_count = w.counters.p + 3;
     a.L = L;
     a.fast_div_ok = o->newton_tol >= 0x1.0p-500;
-    a.relaxed = !strict;
-    a.far32 = !strict && ctx->far32 && (o->flags & CVG_FLAG_NO_FAR32) == 0 && o->variant != CVG_APPROX_TRANSCENDENTAL;
+    // the relaxed path records update counts in 11 bits (queue_redo)
+    a.relaxed = !strict && o->newton_max_iter <= cvg::kRedoMaxIter;
+    a.far32 = a.relaxed && ctx->far32 && (o->flags & CVG_FLAG_NO_FAR32) == 0 && o->variant != CVG_APPROX_TRANSCENDENTAL;
     a.y_win = far_window_limit(o->newton_tol, a.far32);
-    a.tree_precip = !strict && o->variant != CVG_APPROX_TRANSCENDENTAL && o->newton_tol >= 0x1.0p-40;
+    a.tree_precip = a.relaxed && o->variant != CVG_APPROX_TRANSCENDENTAL && o->newton_tol >= 0x1.0p-40;
     a.vec4 = deep->ld % 4 == 0 && aligned32(deep->tend_T) && aligned32(deep->tend_q);
   }
   a.gl_tab = ctx->gl_tab;
@@ -458,7 +483,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     b.d_tend_T = deep->tend_T; b.d_tend_q = deep->tend_q; b.d_precip = deep->precip;
     b.d_work = deep->work_units; b.d_exited = deep->exited_early; b.d_ld_out = deep->ld;
   }
-  b.err = w.err.p + 1; b.gl_tab = ctx->gl_tab; b.first_col = in->first_col;
+  b.err = w.err.p + 1; b.gl_tab = ctx->gl_tab; b.exp_tab1 = ctx->exp_tab1.p; b.first_col = in->first_col;
   b.thr = o->activity_threshold; b.L = L;
   if (ctx->trace_path && &w == &ctx->ws[0]) {
     ctx->trace_d.ensure(3 * 4096);
@@ -473,6 +498,20 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     case 2: launch_kernels<cvg::kVarApprox>(ctx, w, a, b, do_sh, do_deep, pe, st, strict); break;
     default: launch_kernels<cvg::kVarExact>(ctx, w, a, b, do_sh, do_deep, pe, st, strict); break;
   }
+}
+
+void prepare_ws(cvg_context* ctx, Workspace& w, long long n, cudaStream_t st) {
+  const size_t ngroups = (size_t)((n + cvg::kGroupCols - 1) / cvg::kGroupCols);
+  const size_t cap = (size_t)redo_capacity(n);
+  if (w.groups.cap >= ngroups && w.redo.cap >= cvg::kRedoWords * cap && w.fix.cap >= 6 * cap) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CVG_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    throw std::invalid_argument("workspace too small for a call inside a stream capture: make one uncaptured "
+                                "call of this size (or larger) on the context first");
+  w.groups.grow(ngroups, ctx->retired);
+  w.redo.grow(cvg::kRedoWords * cap, ctx->retired);
+  w.fix.grow(6 * cap, ctx->retired);
 }
 
 // Queues the D2H of a workspace's latched failure words / trigger count.
@@ -648,6 +687,7 @@ void cvg_context_free(cvg_context* ctx) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  for (void* p : ctx->retired) cudaFree(p);
   for (auto* b : {&ctx->loop.s, &ctx->loop.oT, &ctx->loop.oq, &ctx->loop.op, &ctx->leg.T, &ctx->leg.q}) b->release();
   ctx->loop.ow.release(); ctx->loop.ox.release(); ctx->loop_err.release(); ctx->loop_flag.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -667,7 +707,7 @@ namespace {
 void launch_graph(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int mask, const cvg_outputs* deep,
                   const cvg_outputs* sh, cudaStream_t st) {
   Workspace& w = ctx->ws[0];
-  if (mask & CVG_DEEP) w.groups.ensure((size_t)((in->n_columns + cvg::kGroupCols - 1) / cvg::kGroupCols));
+  if (mask & CVG_DEEP) prepare_ws(ctx, w, in->n_columns, st);
   std::vector<unsigned char> key;
   auto put = [&](const void* p, size_t n) {
     const unsigned char* b = static_cast<const unsigned char*>(p);
@@ -681,6 +721,8 @@ void launch_graph(cvg_context* ctx, const cvg_columns* in, const cvg_options* o,
   put((mask & CVG_SHALLOW) ? sh : &none, sizeof(none));
   put(&w.groups.p, sizeof(w.groups.p));
   put(&w.groups.cap, sizeof(w.groups.cap));
+  put(&w.redo.p, sizeof(w.redo.p));
+  put(&w.fix.p, sizeof(w.fix.p));
   for (auto& g : ctx->graphs)
     if (g.key == key) {
       CVG_CUDA(cudaGraphLaunch(g.exec, st));
