@@ -228,6 +228,35 @@ cvg_status cvg_plan_partition(long long n, const double* s,
                               double deep_weight, double shallow_weight,
                               long long* bounds);
 
+/* --- Multi-device engine (HeteroEngine::step, hetero.cpp:252-466) ------ */
+
+typedef struct cvg_multi cvg_multi;
+
+/* One context per listed CUDA device (a device may be listed more than once:
+ * independent contexts sharing one GPU).  Partition weights default to the
+ * measured per-unit costs of one B200 (0.83 ns per triggered column, 0.21 ns
+ * per column). */
+cvg_status cvg_multi_create(const int* devices, int n_devices, cvg_multi** out);
+void cvg_multi_free(cvg_multi* m);
+int cvg_multi_size(const cvg_multi* m);
+/* The i-th device context (owned by m), e.g. for device-resident calls. */
+cvg_context* cvg_multi_context(cvg_multi* m, int i);
+/* Cost model of the partition (cvg_plan_partition): deep_weight <= 0 gives
+ * the naive equal-columns split (StaticBlock, sched.cpp:66-75). */
+cvg_status cvg_multi_set_weights(cvg_multi* m, double deep_weight, double shallow_weight);
+
+/* cvg_convect over every device of m, host buffers only: G contiguous column
+ * ranges balanced by the cost model (interior bounds rounded to 32 columns),
+ * each staged over its own device's PCIe link and computed there,
+ * concurrently (one host thread per device).  The outputs equal one
+ * single-device call bit for bit.  stats (nullable) merges the devices:
+ * counts and bytes summed, device_ms the slowest device, the failure the
+ * reference's serial order would report (deep before shallow, lowest
+ * column).  bounds (nullable) receives the G + 1 range offsets. */
+cvg_status cvg_multi_convect(cvg_multi* m, const cvg_columns* in, const cvg_options* opts, int kernel_mask,
+                             const cvg_outputs* deep, const cvg_outputs* shallow, cvg_stats* stats,
+                             long long* bounds);
+
 /* --- Measurement support (bench.py) ----------------------------------- */
 
 /* Per-kernel device timing: while enabled, every cvg_convect_async call

@@ -26,7 +26,7 @@ __all__ = [
     "Variant", "KernelOptions", "KernelError", "DeviceError", "ValidationError", "ColumnOutputs", "Stats",
     "GrowthSeries",
     "Context", "deep_convection", "shallow_convection", "ientropy_solve", "approx_exp",
-    "plan_partition", "library_path", "load_library", "DEEP", "SHALLOW", "BOTH",
+    "plan_partition", "library_path", "load_library", "DEEP", "SHALLOW", "BOTH", "MultiContext",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -169,12 +169,23 @@ def load_library():
     L.cvg_host_free.restype = None
     L.cvg_timestep.argtypes = [vp, i64, i32, i64, vp, vp, vp, i32, C.POINTER(KernelOptions), i32, i32,
                                C.POINTER(Stats)]
+    L.cvg_multi_create.argtypes = [C.POINTER(C.c_int), i32, C.POINTER(vp)]
+    L.cvg_multi_free.argtypes = [vp]
+    L.cvg_multi_free.restype = None
+    L.cvg_multi_size.argtypes = [vp]
+    L.cvg_multi_size.restype = C.c_int
+    L.cvg_multi_context.argtypes = [vp, i32]
+    L.cvg_multi_context.restype = vp
+    L.cvg_multi_set_weights.argtypes = [vp, dbl, dbl]
+    L.cvg_multi_convect.argtypes = [vp, C.POINTER(_Columns), C.POINTER(KernelOptions), i32, C.POINTER(_Outputs),
+                                    C.POINTER(_Outputs), C.POINTER(Stats), vp]
     L.cvg_error_growth.argtypes = [vp, C.POINTER(_Columns), i32, C.POINTER(KernelOptions),
                                    C.POINTER(KernelOptions), i32, vp, vp, C.POINTER(_Growth)]
     for f in ("cvg_profile_begin", "cvg_profile_end", "cvg_fp64_peak", "cvg_host_alloc",
               "cvg_context_create", "cvg_convect", "cvg_convect_async", "cvg_convect_check",
               "cvg_deep_convection", "cvg_shallow_convection", "cvg_ientropy_solve",
-              "cvg_approx_exp", "cvg_plan_partition", "cvg_timestep", "cvg_error_growth"):
+              "cvg_approx_exp", "cvg_plan_partition", "cvg_timestep", "cvg_error_growth",
+              "cvg_multi_create", "cvg_multi_set_weights", "cvg_multi_convect"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -386,6 +397,63 @@ class Context:
         self.last_stats = st
         _raise(rc, st)
         return st
+
+
+class MultiContext:
+    """Several device contexts driven as one (cvg_multi): a host-buffer call
+    is split into contiguous column ranges balanced by estimated cost and
+    run on every device concurrently (the reference's HeteroEngine::step,
+    hetero.cpp:252-466, over G devices).  A device may be listed twice
+    (independent contexts sharing one GPU)."""
+
+    def __init__(self, devices):
+        L = load_library()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _raise(L.cvg_multi_create(devs, len(devices), C.byref(h)))
+        self._h = h
+        self.devices = list(devices)
+        self.last_stats = Stats()
+        self.last_bounds = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().cvg_multi_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_weights(self, deep_weight: float, shallow_weight: float):
+        _raise(load_library().cvg_multi_set_weights(self._h, float(deep_weight), float(shallow_weight)))
+
+    def convect(self, s, T, q, opts: KernelOptions | None = None, kernels=BOTH, first_col=0,
+                out_deep: ColumnOutputs | None = None, out_shallow: ColumnOutputs | None = None):
+        """As Context.convect, over all devices; the range offsets land in
+        ``last_bounds``."""
+        opts = opts or KernelOptions()
+        keep, cols = _host_columns(s, T, q, first_col)
+        L, n = keep[1].shape
+        deep = (out_deep or ColumnOutputs.empty(n, L)) if kernels & DEEP else None
+        sh = (out_shallow or ColumnOutputs.empty(n, L)) if kernels & SHALLOW else None
+        st = Stats()
+        b = np.zeros(len(self.devices) + 1, dtype=np.int64)
+        rc = load_library().cvg_multi_convect(self._h, C.byref(cols), C.byref(opts), kernels,
+                                              C.byref(deep._struct()) if deep else None,
+                                              C.byref(sh._struct()) if sh else None, C.byref(st), b.ctypes.data)
+        self.last_stats = st
+        self.last_bounds = b
+        _raise(rc, st)
+        return deep, sh
 
 
 class PinnedArray:

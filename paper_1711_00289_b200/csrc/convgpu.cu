@@ -20,6 +20,7 @@
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/convgpu.h"
@@ -1352,6 +1353,175 @@ cvg_status cvg_plan_partition(long long n, const double* s, double thr, int n_pa
   while (p < n_parts) bounds[p++] = n;
   bounds[n_parts] = n;
   for (int i = 1; i <= n_parts; ++i) bounds[i] = std::max(bounds[i], bounds[i - 1]);
+  return CVG_OK;
+}
+
+}  // extern "C"
+
+// --- Multi-device engine ------------------------------------------------------
+//
+// The reference's partitioned execution is one call, HeteroEngine::step
+// (hetero.cpp:252-466), over a plan from plan_partition (hetero.cpp:156-176):
+// a host pool and an emulated device each take a contiguous column range.
+// Here G device contexts each take one contiguous range, balanced by the
+// estimated cost w_c = deep_weight [s_c > thr] + shallow_weight
+// (cvg_plan_partition), and run concurrently, one host thread per device,
+// each staging its range over its own PCIe link (cvg_convect).  Columns are
+// independent (physics.hpp:26-30), so the ranges need no exchange: the union
+// of the G outputs equals one single-device call bit for bit.
+
+struct cvg_multi {
+  std::vector<cvg_context*> ctx;
+  double deep_weight = 0.83;     // measured ns per triggered column (multigpu.py)
+  double shallow_weight = 0.21;  // measured ns per column
+};
+
+namespace {
+
+// Interior offsets rounded to multiples of 32 columns (each range's rows then
+// start on 256-byte boundaries in the staging buffers), kept monotone.
+void align_bounds(long long* b, int parts, long long n) {
+  for (int i = 1; i < parts; ++i) {
+    long long r = (b[i] + 16) / 32 * 32;
+    b[i] = std::min(n, std::max(b[i - 1], r));
+  }
+  b[parts] = n;
+}
+
+}  // namespace
+
+extern "C" {
+
+cvg_status cvg_multi_create(const int* devices, int n_devices, cvg_multi** out) {
+  if (!out || !devices) return fail(CVG_ERR_INVALID, "cvg_multi_create: null argument");
+  *out = nullptr;
+  if (n_devices < 1 || n_devices > 64) return fail(CVG_ERR_INVALID, "cvg_multi_create: n_devices must be in [1, 64]");
+  auto* m = new cvg_multi();
+  for (int i = 0; i < n_devices; ++i) {
+    cvg_context* c = nullptr;
+    const cvg_status st = cvg_context_create(devices[i], &c);
+    if (st != CVG_OK) {
+      const std::string msg = cvg_last_error();
+      cvg_multi_free(m);
+      return fail(st, "cvg_multi_create: device " + std::to_string(devices[i]) + ": " + msg);
+    }
+    m->ctx.push_back(c);
+  }
+  g_last_error.clear();
+  *out = m;
+  return CVG_OK;
+}
+
+void cvg_multi_free(cvg_multi* m) {
+  if (!m) return;
+  for (cvg_context* c : m->ctx) cvg_context_free(c);
+  delete m;
+}
+
+int cvg_multi_size(const cvg_multi* m) { return m ? (int)m->ctx.size() : 0; }
+
+cvg_context* cvg_multi_context(cvg_multi* m, int i) {
+  if (!m || i < 0 || i >= (int)m->ctx.size()) return nullptr;
+  return m->ctx[i];
+}
+
+cvg_status cvg_multi_set_weights(cvg_multi* m, double deep_weight, double shallow_weight) {
+  if (!m) return fail(CVG_ERR_INVALID, "cvg_multi_set_weights: null handle");
+  if (!(shallow_weight >= 0.0) || !std::isfinite(deep_weight))
+    return fail(CVG_ERR_INVALID, "cvg_multi_set_weights: bad weights");
+  m->deep_weight = deep_weight;
+  m->shallow_weight = shallow_weight;
+  g_last_error.clear();
+  return CVG_OK;
+}
+
+cvg_status cvg_multi_convect(cvg_multi* m, const cvg_columns* in, const cvg_options* opts, int mask,
+                             const cvg_outputs* deep, const cvg_outputs* sh, cvg_stats* stats,
+                             long long* bounds_out) {
+  if (!m || !in || !opts) return fail(CVG_ERR_INVALID, "cvg_multi_convect: null argument");
+  std::string why;
+  if (!valid_columns(in, &why) || !valid_options(opts, &why)) return fail(CVG_ERR_INVALID, "cvg_multi_convect: " + why);
+  if (mask < 1 || mask > 3) return fail(CVG_ERR_INVALID, "cvg_multi_convect: kernel_mask must be 1, 2 or 3");
+  if ((mask & CVG_DEEP) && (!deep || !valid_outputs(deep, in->n_columns, &why)))
+    return fail(CVG_ERR_INVALID, "cvg_multi_convect: deep outputs: " + (deep ? why : std::string("null")));
+  if ((mask & CVG_SHALLOW) && (!sh || !valid_outputs(sh, in->n_columns, &why)))
+    return fail(CVG_ERR_INVALID, "cvg_multi_convect: shallow outputs: " + (sh ? why : std::string("null")));
+  if (in->on_device || ((mask & CVG_DEEP) && deep->on_device) || ((mask & CVG_SHALLOW) && sh->on_device))
+    return fail(CVG_ERR_INVALID,
+                "cvg_multi_convect: host buffers only (device-resident ranges: cvg_convect_async on each "
+                "cvg_multi_context)");
+  const int G = (int)m->ctx.size();
+  const long long n = in->n_columns;
+  std::vector<long long> b(G + 1, 0);
+  cvg_status rc = cvg_plan_partition(n, in->s, opts->activity_threshold, G, m->deep_weight, m->shallow_weight,
+                                     b.data());
+  if (rc != CVG_OK) return rc;
+  align_bounds(b.data(), G, n);
+  if (bounds_out) std::copy(b.begin(), b.end(), bounds_out);
+  struct Part {
+    cvg_status rc = CVG_OK;
+    cvg_stats st{};
+    std::string msg;
+  };
+  std::vector<Part> parts(G);
+  auto run = [&](int i) {
+    const long long c0 = b[i], m_i = b[i + 1] - b[i];
+    cvg_columns ci = *in;
+    ci.n_columns = m_i;
+    ci.first_col = in->first_col + c0;
+    ci.s = in->s + c0;
+    ci.T = in->T + c0;
+    ci.q = in->q + c0;
+    auto slice = [&](const cvg_outputs* o) {
+      cvg_outputs d = *o;
+      d.tend_T += c0; d.tend_q += c0; d.precip += c0; d.work_units += c0; d.exited_early += c0;
+      return d;
+    };
+    cvg_outputs dd{}, ds{};
+    if (mask & CVG_DEEP) dd = slice(deep);
+    if (mask & CVG_SHALLOW) ds = slice(sh);
+    parts[i].rc = cvg_convect(m->ctx[i], &ci, opts, mask, (mask & CVG_DEEP) ? &dd : nullptr,
+                              (mask & CVG_SHALLOW) ? &ds : nullptr, &parts[i].st);
+    if (parts[i].rc != CVG_OK) parts[i].msg = cvg_last_error();
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < G; ++i) th.emplace_back(run, i);
+  run(0);
+  for (auto& t : th) t.join();
+  // merge: the reference reports the first failure of its serial order --
+  // deep before shallow, then the lowest column; ranges are in column order
+  int pick = -1;
+  for (int pass = 0; pass < 2 && pick < 0; ++pass) {
+    const int kern = pass == 0 ? CVG_DEEP : CVG_SHALLOW;
+    for (int i = 0; i < G; ++i)
+      if (parts[i].rc == CVG_ERR_NUMERIC && parts[i].st.failing_kernel == kern) { pick = i; break; }
+  }
+  if (pick < 0)
+    for (int i = 0; i < G; ++i)
+      if (parts[i].rc != CVG_OK) { pick = i; break; }
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->n_columns = n;
+    stats->failing_column = -1;
+    for (int i = 0; i < G; ++i) {
+      const cvg_stats& s = parts[i].st;
+      stats->n_triggered += s.n_triggered;
+      stats->n_recomputed += s.n_recomputed;
+      stats->n_corrected += s.n_corrected;
+      stats->h2d_bytes += s.h2d_bytes;
+      stats->d2h_bytes += s.d2h_bytes;
+      stats->device_ms = std::max(stats->device_ms, s.device_ms);
+      stats->h2d_ms = std::max(stats->h2d_ms, s.h2d_ms);
+      stats->d2h_ms = std::max(stats->d2h_ms, s.d2h_ms);
+    }
+    if (pick >= 0) {
+      stats->failing_column = parts[pick].st.failing_column;
+      stats->failure_kind = parts[pick].st.failure_kind;
+      stats->failing_kernel = parts[pick].st.failing_kernel;
+    }
+  }
+  if (pick >= 0) return fail(parts[pick].rc, parts[pick].msg);
+  g_last_error.clear();
   return CVG_OK;
 }
 

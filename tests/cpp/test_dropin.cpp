@@ -130,6 +130,44 @@ int main() {
     }
     CHECK(thrown);
   }
+  {  // the multi-device engine (HeteroEngine::step over G devices): a 4-way
+     // split -- one GPU listed four times on a one-GPU box -- equals the
+     // single-device call bit for bit and the reference within its rule
+    GridSpec spec;
+    spec.n_columns = 50000;
+    spec.seed = 21;
+    const Chunk grid = make_grid(spec);
+    cvg::MultiSession multi({0, 0, 0, 0});
+    const auto want = deep_convection(grid, exact);
+    const auto one = gpu.deep_convection<ColumnOutput, KernelError>(grid, exact);
+    const auto four = multi.deep_convection<ColumnOutput, KernelError>(grid, exact);
+    long long differ = 0, off = 0;
+    for (size_t i = 0; i < want.size(); ++i) {
+      if (!bitwise(one[i], four[i])) ++differ;
+      if (!close_fields(four[i], want[i]) || four[i].work_units != want[i].work_units) ++off;
+    }
+    CHECK(differ == 0);
+    CHECK(off == 0);
+    const auto& b = multi.last_bounds();
+    CHECK(b.size() == 5 && b.front() == 0 && b.back() == 50000);
+    for (size_t i = 1; i + 1 < b.size(); ++i) CHECK(b[i] % 32 == 0 && b[i] > b[i - 1]);
+    CHECK(multi.last_stats().n_triggered == gpu.last_stats().n_triggered);
+    CHECK(multi.last_marshal_ms() > 0.0);
+    std::printf("multi: bounds %lld %lld %lld %lld %lld, marshal %.2f ms, device %.2f ms\n", b[0], b[1], b[2], b[3],
+                b[4], multi.last_marshal_ms(), multi.last_stats().device_ms);
+    Chunk bad = grid;   // failures in two ranges: the lowest column is reported
+    for (auto& c : bad.cols) c.s = 0.9;
+    bad.cols[41000].T[2] = std::nan("");
+    bad.cols[9000].T[7] = std::nan("");
+    bool thrown = false;
+    try {
+      multi.deep_convection<ColumnOutput, KernelError>(bad, exact);
+    } catch (const KernelError& e) {
+      thrown = true;
+      CHECK(e.column() == 9000);
+    }
+    CHECK(thrown);
+  }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "PASSED", g_fail);
   return g_fail ? 1 : 0;
 }

@@ -116,3 +116,19 @@ def test_overlap_partition_minimises_the_largest_share():
         lin = P.plan_partition(s, 0.5, world, *multigpu.partition_weights())
         assert ov[0] == 0 and ov[-1] == s.size and np.all(np.diff(ov) >= 0)
         assert cost(ov) <= cost(lin) + 1e-12
+
+
+def test_multi_engine_conventions_without_device():
+    """cvg_multi: null/size checks, and no CPU fallback without a device."""
+    lib = P.load_library()
+    h = C.c_void_p()
+    assert lib.cvg_multi_create(None, 1, C.byref(h)) == 1
+    assert b"null" in lib.cvg_last_error()
+    assert lib.cvg_multi_create((C.c_int * 2)(0, 0), 0, C.byref(h)) == 1
+    assert lib.cvg_multi_size(None) == 0
+    assert lib.cvg_multi_context(None, 0) is None
+    assert lib.cvg_multi_set_weights(None, 1.0, 1.0) == 1
+    import torch
+    if not torch.cuda.is_available():
+        with pytest.raises(P.DeviceError):
+            P.MultiContext([0, 0])
