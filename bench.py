@@ -442,9 +442,10 @@ def run_gpu_arm(args):
         a2, a42 = min(loop_s(2) for _ in range(3)), min(loop_s(42) for _ in range(3))
         per = (a42 - a2) / 40
         loop = None if per <= 0 else {"kernel": "deep", "ms_per_step": 1e3 * per, "columns_per_s": n_total / per,
-                "note": "cvg_timestep: deep kernel + advance (T += tend_T, q += tend_q) + check_finite per step, "
-                        "state resident in HBM; (t(42 steps) - t(2 steps)) / 40, wall clock incl. the per-step "
-                        "divergence check"}
+                "note": "cvg_timestep: per step the deep kernel advances the state in place (T += tend_T, "
+                        "q += tend_q) with check_finite latched on the device, guard-band re-derivation applied "
+                        "to the state; the host checks every 16 steps (first failing step reported); state "
+                        "resident in HBM; (t(42 steps) - t(2 steps)) / 40, wall clock"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

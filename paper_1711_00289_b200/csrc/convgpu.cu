@@ -301,13 +301,22 @@ void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
   CVG_CUDA(cudaGetLastError());
 }
 
+// Feedback-loop mode of a call (cvg_timestep): the kernels write the
+// advanced state in place instead of tendency rows (DeepArgs::adv_T).
+struct Fused {
+  double* T;
+  double* q;
+  unsigned* bad;
+};
+
 // deep kernel on `st`, then the shallow(+zero-fill) kernel: concurrently on
 // the workspace's side stream in overlap mode (the FP64-bound and the
 // HBM-bound kernel share the SMs), else after it on `st`.
 template <int VAR>
 void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh,
-                    bool dp, cudaEvent_t* pe, cudaStream_t st, bool strict) {
-  const bool ov = ctx->overlap && dp;
+                    bool dp, cudaEvent_t* pe, cudaStream_t st, bool strict, bool fused) {
+  // overlap layout only when a shallow (or zero-fill) kernel shares the SMs
+  const bool ov = ctx->overlap && dp && (sh || !fused);
   const cudaStream_t main = st;
   if (ov) CVG_CUDA(cudaEventRecord(w.ev_fork, st));
   // Thread-per-column deep kernel for large calls (the f02 grid on one or
@@ -323,7 +332,8 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // thread per column, CVG_DEEP_LPC=0 the warp-per-column kernel,
   // CVG_DEEP_LPC=2/4 the split width.
   const bool tpc_forced = ctx->deep_tpc == 1;
-  const int lpc_n = ctx->deep_lpc >= 0 ? ctx->deep_lpc : (a.n >= cvg::kTpcMinColumns / 2 ? 2 : 4);
+  int lpc_n = ctx->deep_lpc >= 0 ? ctx->deep_lpc : (a.n >= cvg::kTpcMinColumns / 2 ? 2 : 4);
+  if (fused && lpc_n <= 1 && !tpc_forced) lpc_n = 2;   // the warp-per-column kernel has no feedback-loop mode
   const bool lpc = !tpc_forced && dp && lpc_n > 1;
   const bool tpc = !lpc && dp && a.L <= 32 &&
                    (tpc_forced || (ctx->deep_tpc == 2 && a.n >= cvg::kTpcMinColumns));
@@ -390,7 +400,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
       k = cvg::shallow_kernel<VAR, true, true>;
     } else if (sh) {
       k = cvg::shallow_kernel<VAR, true, false>;
-    } else if (dp) {
+    } else if (dp && !fused) {   // (the feedback loop leaves untriggered columns untouched)
       k = cvg::shallow_kernel<VAR, false, true>;
     }
     if (k) {
@@ -418,17 +428,23 @@ long long redo_capacity(long long n) { return std::min<long long>(n / 2 + 4096, 
 // being captured (a caller's graph) is refused: allocation is not capturable
 // and the graph would bake in the size -- size the workspace with one
 // uncaptured call first.
-void prepare_ws(cvg_context* ctx, Workspace& w, long long n, cudaStream_t st);
+void prepare_ws(cvg_context* ctx, Workspace& w, long long n, long long cap, cudaStream_t st);
 
 // Enqueues the hot path on `st` with workspace `w`: memsets of the per-call
 // cursors and failure words, the trigger + compaction kernel (deep
 // requested), then the deep and shallow kernels.  Pointers are device
 // pointers.  pe: optional 4 profiling events.
 void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_options* o, int mask,
-             const cvg_outputs* deep, const cvg_outputs* sh, cudaStream_t st, cudaEvent_t* pe) {
+             const cvg_outputs* deep, const cvg_outputs* sh, cudaStream_t st, cudaEvent_t* pe,
+             const Fused* fu = nullptr) {
   const long long n = in->n_columns;
   const int L = in->n_levels;
-  if (ctx->reset_kernel) {
+  // the redo list: every level fits in the feedback-loop mode (its in-place
+  // state cannot be recomputed from the inputs after an overflow)
+  const long long cap = fu ? std::min<long long>(n * L, 0x3fffffffLL) : redo_capacity(n);
+  if (fu) {
+    // per-call words: reset by the previous step's step_end_kernel
+  } else if (ctx->reset_kernel) {
     cvg::reset_call_words_kernel<<<1, 32, 0, st>>>(w.counters.p, 4, w.cursor.p, 20, w.err.p, 2);
     CVG_CUDA(cudaGetLastError());
   } else {
@@ -439,7 +455,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
   if (n == 0) return;
   const bool do_deep = (mask & CVG_DEEP) != 0, do_sh = (mask & CVG_SHALLOW) != 0;
   const bool strict = ctx->strict || (o->flags & CVG_FLAG_STRICT) != 0;
-  if (do_deep) prepare_ws(ctx, w, n, st);
+  if (do_deep) prepare_ws(ctx, w, n, cap, st);
   if (pe) CVG_CUDA(cudaEventRecord(pe[0], st));
   cvg::DeepArgs a{};
   if (do_deep) {
@@ -459,7 +475,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.redo = w.redo.p;
     a.fix = w.fix.p;
     a.blocks_done = reinterpret_cast<unsigned*>(w.cursor.p + 16);   // reset per call
-    a.redo_cap = (int)redo_capacity(n);
+    a.redo_cap = (int)cap;
     a.redo_count = w.counters.p + 2;
     a.fix_count = w.counters.p + 3;
     a.L = L;
@@ -473,6 +489,9 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
   }
   a.gl_tab = ctx->gl_tab;
   a.exp_tab1 = ctx->exp_tab1.p;
+  if (fu) {
+    a.adv_T = fu->T; a.adv_q = fu->q; a.adv_bad = fu->bad;
+  }
   if (pe) CVG_CUDA(cudaEventRecord(pe[1], st));
   cvg::ShallowArgs b{};
   b.s = in->s; b.T = in->T; b.q = in->q; b.ld_in = in->ld; b.n = n;
@@ -486,6 +505,9 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
   }
   b.err = w.err.p + 1; b.gl_tab = ctx->gl_tab; b.exp_tab1 = ctx->exp_tab1.p; b.first_col = in->first_col;
   b.thr = o->activity_threshold; b.L = L;
+  if (fu) {
+    b.adv_T = fu->T; b.adv_q = fu->q; b.adv_bad = fu->bad;
+  }
   if (ctx->trace_path && &w == &ctx->ws[0]) {
     ctx->trace_d.ensure(3 * 4096);
     ctx->trace_s.ensure(3 * (size_t)((n + 127) / 128 + 1));
@@ -495,15 +517,15 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     b.trace = ctx->trace_s.p;
   }
   switch (o->variant) {
-    case 1: launch_kernels<cvg::kVarReduced>(ctx, w, a, b, do_sh, do_deep, pe, st, strict); break;
-    case 2: launch_kernels<cvg::kVarApprox>(ctx, w, a, b, do_sh, do_deep, pe, st, strict); break;
-    default: launch_kernels<cvg::kVarExact>(ctx, w, a, b, do_sh, do_deep, pe, st, strict); break;
+    case 1: launch_kernels<cvg::kVarReduced>(ctx, w, a, b, do_sh, do_deep, pe, st, strict, fu != nullptr); break;
+    case 2: launch_kernels<cvg::kVarApprox>(ctx, w, a, b, do_sh, do_deep, pe, st, strict, fu != nullptr); break;
+    default: launch_kernels<cvg::kVarExact>(ctx, w, a, b, do_sh, do_deep, pe, st, strict, fu != nullptr); break;
   }
 }
 
-void prepare_ws(cvg_context* ctx, Workspace& w, long long n, cudaStream_t st) {
+void prepare_ws(cvg_context* ctx, Workspace& w, long long n, long long cap_, cudaStream_t st) {
   const size_t ngroups = (size_t)((n + cvg::kGroupCols - 1) / cvg::kGroupCols);
-  const size_t cap = (size_t)redo_capacity(n);
+  const size_t cap = (size_t)cap_;
   if (w.groups.cap >= ngroups && w.redo.cap >= cvg::kRedoWords * cap && w.fix.cap >= 6 * cap) return;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   CVG_CUDA(cudaStreamIsCapturing(st, &cs));
@@ -708,7 +730,7 @@ namespace {
 void launch_graph(cvg_context* ctx, const cvg_columns* in, const cvg_options* o, int mask, const cvg_outputs* deep,
                   const cvg_outputs* sh, cudaStream_t st) {
   Workspace& w = ctx->ws[0];
-  if (mask & CVG_DEEP) prepare_ws(ctx, w, in->n_columns, st);
+  if (mask & CVG_DEEP) prepare_ws(ctx, w, in->n_columns, redo_capacity(in->n_columns), st);
   std::vector<unsigned char> key;
   auto put = [&](const void* p, size_t n) {
     const unsigned char* b = static_cast<const unsigned char*>(p);
@@ -1168,35 +1190,58 @@ cvg_status cvg_timestep(cvg_context* ctx, long long n, int L, long long ld, cons
     cudaStream_t st = ctx->stream;
     LoopBufs& lb = ctx->loop;
     LegBufs& leg = ctx->leg;
-    DevBuf<unsigned long long>& err = ctx->loop_err;
-    DevBuf<unsigned>& flag = ctx->loop_flag;
+    // Fused loop: every step is trigger -> kernel (writing the advanced
+    // state in place, with the check_finite flag) -> re-derivation ->
+    // step_end (the step's failure words and flag saved in slot t % K); the
+    // host synchronises once per K steps and reports the first failing step
+    // as the reference's per-step checks would (validate.cpp:127-153).
+    constexpr int K = 16;
+    DevBuf<unsigned long long>& slots = ctx->loop_err;   // [K][2] failure words
+    DevBuf<unsigned>& words = ctx->loop_flag;            // [0] flag, [1] step, [2..2+K) flags per slot
     lb.ensure(std::max(n, 1LL), L);
     leg.T.ensure((size_t)std::max(n, 1LL) * L);
     leg.q.ensure((size_t)std::max(n, 1LL) * L);
-    err.ensure(2);
-    flag.ensure(1);
+    slots.ensure(2 * K);
+    words.ensure(2 + K);
     const cudaMemcpyKind kin = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const cudaMemcpyKind kout = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    Workspace& w = ctx->ws[0];
     if (n > 0) {
       CVG_CUDA(cudaMemcpyAsync(lb.s.p, s, sizeof(double) * n, kin, st));
       CVG_CUDA(cudaMemcpy2DAsync(leg.T.p, sizeof(double) * n, T, sizeof(double) * ld, sizeof(double) * n, L, kin, st));
       CVG_CUDA(cudaMemcpy2DAsync(leg.q.p, sizeof(double) * n, q, sizeof(double) * ld, sizeof(double) * n, L, kin, st));
     }
-    CVG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(unsigned), st));
-    cvg_status rc = CVG_OK;
-    for (int t = 0; t < n_steps && n > 0; ++t) {
-      leg_step(ctx, opts, kernel, n, L, lb.s.p, leg, lb, err.p, flag.p, st);
-      unsigned long long h_err[2];
-      unsigned h_flag = 0;
-      CVG_CUDA(cudaMemcpyAsync(h_err, err.p, sizeof(h_err), cudaMemcpyDeviceToHost, st));
-      CVG_CUDA(cudaMemcpyAsync(&h_flag, flag.p, sizeof(h_flag), cudaMemcpyDeviceToHost, st));
-      CVG_CUDA(cudaStreamSynchronize(st));
-      rc = leg_errors(h_err, 1, kernel, opts->newton_max_iter, n);
-      if (rc != CVG_OK) {
-        if (stats) stats->failing_column = (long long)(std::min(h_err[0], h_err[1]) >> 16);
-        return rc;
+    CVG_CUDA(cudaMemsetAsync(words.p, 0, (2 + K) * sizeof(unsigned), st));
+    cvg::reset_call_words_kernel<<<1, 32, 0, st>>>(w.counters.p, 4, w.cursor.p, 20, w.err.p, 2);
+    if (n > 0) {   // the initial state's non-finite values (columns the steps never touch)
+      cvg::nonfinite_scan_kernel<<<ctx->num_sms * 4, 256, 0, st>>>(leg.T.p, leg.q.p, n, n, L, words.p);
+    }
+    CVG_CUDA(cudaGetLastError());
+    const cvg_columns in{n, L, 0, n, lb.s.p, leg.T.p, leg.q.p, 1};
+    const cvg_outputs out = lb.outs(n);
+    const Fused fu{leg.T.p, leg.q.p, words.p};
+    std::vector<unsigned long long> h_err(2 * K);
+    std::vector<unsigned> h_bad(K);
+    for (int t0 = 0; t0 < n_steps && n > 0; t0 += K) {
+      const int kk = std::min(K, n_steps - t0);
+      for (int j = 0; j < kk; ++j) {
+        enqueue(ctx, w, &in, opts, kernel, kernel == CVG_DEEP ? &out : nullptr, kernel == CVG_SHALLOW ? &out : nullptr,
+                st, nullptr, &fu);
+        cvg::step_end_kernel<<<1, 32, 0, st>>>(words.p + 1, w.counters.p, w.cursor.p, w.err.p, words.p, slots.p,
+                                               words.p + 2, K);
+        CVG_CUDA(cudaGetLastError());
       }
-      if (h_flag) return fail(CVG_ERR_CHECK, "timestep: state diverged at step " + std::to_string(t));
+      CVG_CUDA(cudaMemcpyAsync(h_err.data(), slots.p, sizeof(unsigned long long) * 2 * K, cudaMemcpyDeviceToHost, st));
+      CVG_CUDA(cudaMemcpyAsync(h_bad.data(), words.p + 2, sizeof(unsigned) * K, cudaMemcpyDeviceToHost, st));
+      CVG_CUDA(cudaStreamSynchronize(st));
+      for (int j = 0; j < kk; ++j) {   // step t0 + j sits in slot (t0 + j) % K = j
+        const cvg_status rc = leg_errors(&h_err[2 * j], 1, kernel, opts->newton_max_iter, n);
+        if (rc != CVG_OK) {
+          if (stats) stats->failing_column = (long long)(std::min(h_err[2 * j], h_err[2 * j + 1]) >> 16);
+          return rc;
+        }
+        if (h_bad[j]) return fail(CVG_ERR_CHECK, "timestep: state diverged at step " + std::to_string(t0 + j));
+      }
     }
     if (n > 0) {
       CVG_CUDA(cudaMemcpy2DAsync(T, sizeof(double) * ld, leg.T.p, sizeof(double) * n, sizeof(double) * n, L, kout, st));

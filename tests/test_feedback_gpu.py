@@ -36,6 +36,34 @@ def test_timestep_equals_convect_plus_host_advance(ctx, kernel):
     assert np.array_equal(T, G.make_config("c1", n=700, seed=21)[1])   # input untouched
 
 
+@pytest.mark.parametrize("kernel", [P.DEEP, P.SHALLOW])
+def test_fused_loop_over_many_steps_equals_convect_plus_advance(ctx, kernel):
+    """More steps than the loop's check interval (16): the fused steps (state
+    advanced in place by the kernels, guard-band patches applied to the
+    state) equal convect + host advance bit for bit."""
+    s, T, q = G.make_config("c4", shape=(48, 96), seed=23)
+    T1, q1 = T.copy(), q.copy()
+    for _ in range(35):
+        deep, sh = ctx.convect(s, T1, q1, kernels=kernel)
+        o = deep if kernel == P.DEEP else sh
+        T1 = T1 + o.tend_T
+        q1 = q1 + o.tend_q
+    T2, q2 = ctx.timestep(s, T, q, kernel=kernel, n_steps=35)
+    assert np.array_equal(T1, T2) and np.array_equal(q1, q2)
+
+
+def test_fused_loop_checks_untouched_columns_at_step_0(ctx):
+    """A NaN in a column the deep kernel leaves alone (s <= threshold): the
+    reference's check_finite fails after step 0's advance (T + 0 = NaN)."""
+    s, T, q = G.make_config("c1", n=512, seed=4)
+    cold = int(np.nonzero(s <= 0.5)[0][3])
+    T = T.copy()
+    T[7, cold] = np.nan
+    with pytest.raises(P.ValidationError) as e:
+        ctx.timestep(s, T, q, kernel=P.DEEP, n_steps=20)
+    assert "step 0" in str(e.value)
+
+
 def test_timestep_matches_oracle_loop(ctx):
     s, T, q = G.make_config("c2", n=2000, seed=5)
     T1, q1 = T.copy(), q.copy()
