@@ -183,6 +183,68 @@ def cpu_baseline(s, T, q, thr, variant, target_s=10.0):
             "sample": f"every {stride}th column ({ss.size} columns), serial C oracle", "wall_s": wall}
 
 
+def workload_config(args, n_columns, levels, thr):
+    """The `config` dict -- identical in both arms (the driver compares it)."""
+    return {"workload": args.config, "n_columns": int(n_columns), "levels": int(levels),
+            "activity_threshold": float(thr), "variant": int(args.variant)}
+
+
+def serial_reference(s, T, q, thr, variant, target_s=2.0):
+    """The reference's serial chunk drivers deep_convection + shallow_convection
+    (physics.cpp:227-245) on one core, on a strided sample (BASELINE.md 2:
+    the serial number beside run_parallel); median of 3."""
+    import oracle as O
+    opts = O.Options(variant=variant, activity_threshold=thr)
+    stride = max(1, s.size // 20000)
+    cs, cT, cq = strided_sample(s, T, q, stride)
+    t0 = time.perf_counter()
+    O.ref_convection("deep", cs, cT, cq, opts)
+    O.ref_convection("shallow", cs, cT, cq, opts)
+    rate = cs.size / max(time.perf_counter() - t0, 1e-6)
+    stride = max(1, s.size // int(min(s.size, max(2000, rate * target_s))))
+    ss, sT, sq = strided_sample(s, T, q, stride)
+    walls = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        O.ref_convection("deep", ss, sT, sq, opts)
+        O.ref_convection("shallow", ss, sT, sq, opts)
+        walls.append(time.perf_counter() - t0)
+    wall = float(np.median(walls))
+    return {"value": ss.size / wall, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"every {stride}th column ({ss.size} columns), reference serial deep_convection + "
+                      f"shallow_convection, median of 3"}
+
+
+def parity_against_reference(s, T, q, thr, variant, deep, sh, stats):
+    """The step's outputs (full grid) against the reference's own run_parallel
+    outputs on the same grid (the north star's rule: flags and work_units
+    exact, fp64 fields within 1e-10 relative or 1e-14 absolute)."""
+    import oracle as O
+    opts = O.Options(variant=variant, activity_threshold=thr)
+    rec = {"columns": int(s.size), "rule": "flags and work_units exact; tend_T, tend_q, precip within 1e-10 "
+                                           "relative or 1e-14 absolute; every column, no exemption",
+           "exempt_columns": 0, "rederived_levels": int(stats.n_recomputed),
+           "rewritten_patches": int(stats.n_corrected)}
+    ok = True
+    for kernel, got in (("deep", deep), ("shallow", sh)):
+        ref, _ = O.ref_run_parallel(kernel, s, T, q, opts)
+        flags = int((got[4] != ref.exited).sum())
+        work = int((got[3] != ref.work).sum())
+        viol, worst = 0, 0.0
+        for a, b in ((got[0], ref.tend_T), (got[1], ref.tend_q), (got[2], ref.precip)):
+            d = np.abs(a - b)
+            viol += int((d > np.maximum(1e-10 * np.abs(b), 1e-14)).sum())
+            nz = np.abs(b) > 0
+            if nz.any():
+                worst = max(worst, float((d[nz] / np.abs(b[nz])).max()))
+        rec[kernel] = {"flag_mismatch": flags, "work_mismatch": work, "tolerance_violations": viol,
+                       "max_rel_err": worst}
+        ok = ok and flags == 0 and work == 0 and viol == 0
+    rec["work_mismatch"] = rec["deep"]["work_mismatch"] + rec["shallow"]["work_mismatch"]
+    rec["ok"] = ok
+    return rec
+
+
 # ---------------------------------------------------------------------------
 def run_reference_arm(args):
     ws, rank, local = dist_env()
@@ -225,8 +287,7 @@ def run_reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(walls),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, gridgen.py)",
-        "config": {"workload": args.config, "n_columns_sample": int(ss.size), "levels": int(T.shape[0]),
-                   "activity_threshold": thr, "variant": args.variant},
+        "config": workload_config(args, s.size, T.shape[0], thr),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -319,6 +380,28 @@ def run_gpu_arm(args):
     if dist:
         dist.barrier()
     ms_local = ev0.elapsed_time(ev1)
+    step_stats = ctx.check(stream)
+    deep_kernel = ctx.last_deep_kernel
+
+    def timed_pass(o, k=K):   # ms per step of k steps with options o (untimed by the contract)
+        for _ in range(2):
+            ctx.convect_async(ds, dT, dq, deep_o, sh_o, o, P.BOTH, first_col=lo, stream=stream)
+        ev0.record(stream)
+        for _ in range(k):
+            ctx.convect_async(ds, dT, dq, deep_o, sh_o, o, P.BOTH, first_col=lo, stream=stream)
+        ev1.record(stream)
+        stream.synchronize()
+        ctx.check(stream)
+        return ev0.elapsed_time(ev1) / k
+
+    # median of >= 5 repetitions of the same K-step region
+    reps5 = [timed_pass(opts) for _ in range(5)]
+    # the exactness trade beside the headline: the same step without the FP32
+    # far phase, and with the reference's rounding in every Newton update
+    paths_ms = {"default": float(np.median(reps5)),
+                "no_far32": timed_pass(P.KernelOptions(variant=args.variant, activity_threshold=thr, far32=False)),
+                "strict": timed_pass(P.KernelOptions(variant=args.variant, activity_threshold=thr, strict=True))}
+    step()   # outputs of the default path for the model counts and the parity check
     ctx.check(stream)
     if os.environ.get("BENCH_DEBUG"):   # diagnostic: three more timed passes to stderr (run-to-run spread)
         print(f"debug: lo={lo} hi={hi} n={n} ms/step={ms_local / K:.4f}", file=sys.stderr)
@@ -373,7 +456,8 @@ def run_gpu_arm(args):
         try:
             with open(tf) as f:
                 d = json.load(f)
-            if d.get("config") == args.config and ws == 1:
+            # only for the kernel this run launched, profiled on this workload
+            if d.get("config") == args.config and d.get("kernel_desc") == deep_kernel and ws == 1 and not args.slice:
                 traffic = d.get("dram_bytes_per_launch")
         except Exception:
             pass
@@ -448,21 +532,32 @@ def run_gpu_arm(args):
                         "resident in HBM; (t(42 steps) - t(2 steps)) / 40, wall clock"}
 
     cpu = None
+    parity = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_baseline(s, T, q, thr, args.variant)
+        import oracle as O
+        if O.ref_available():
+            cpu["serial"] = serial_reference(s, T, q, thr, args.variant)
+            host = lambda o: [t.cpu().numpy() for t in o]   # noqa: E731
+            parity = parity_against_reference(s, T, q, thr, args.variant, host(deep_o), host(sh_o), step_stats)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded counter-based generator, paper_1711_00289_b200/gridgen.py)",
-        "config": {"workload": args.config, "n_columns": int(n_total), "levels": int(L),
-                   "activity_threshold": thr, "variant": args.variant,
-                   "triggered_deep": int(n_trig), "partition": args.partition if ws > 1 else "single",
-                   "l2": "inputs (425 MB) + outputs (880 MB) exceed the 126 MB L2; no flush needed",
-                   "parallelism": f"column partition x{ws}, no collective"},
+        "config": workload_config(args, n_total, L, thr),
+        "workload_notes": {"triggered_deep": int(n_trig), "partition": args.partition if ws > 1 else "single",
+                           "l2": "inputs (432 MB) + outputs (879 MB) exceed the 126 MB L2; no flush needed",
+                           "parallelism": f"column partition x{ws}, no collective"},
+        "ms_per_step_median_of_5": paths_ms["default"],
+        "paths_ms_per_step": {**paths_ms, "note": "default = relaxed Newton update with FP32 far phase and the "
+                                                  "guard-band re-derivation (work_units exact); no_far32 = FP64 "
+                                                  "relaxed update only; strict = the reference's rounding in every "
+                                                  "update (bit-identical roots and counts)"},
+        "parity": parity,
         "roofline": {"bound": "fp64",
-                     "kernel": "deep_tpc_kernel" if n >= 320000 else "deep_kernel",
+                     "kernel": deep_kernel,
                      "achieved": achieved,
                      "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                      "traffic": traffic,
@@ -476,12 +571,14 @@ def run_gpu_arm(args):
                           "fp64_peak_tflops": fp64_peak,
                           "bound": "fp64" if t_flop >= t_hbm else "hbm",
                           "roofline_ms": 1e3 * t_roof, "frac": 1e3 * t_roof / (ms_total / K),
+                          "frac_fp64_model": 1e3 * t_flop / (ms_total / K), "frac_hbm": 1e3 * t_hbm / (ms_total / K),
                           "note": "job FLOPs and bytes over all ranks / N GPUs; frac = roofline time / max-over-ranks step time"},
         "kernels_ms": {"trigger_groups": trig_ms, "deep": deep_ms, "shallow_tail_after_deep": sh_ms,
                        "schedule": "trigger/group compaction -> deep (main stream) || shallow + zero-fill of "
                                    "untriggered groups (side stream, concurrent)"},
-        # per step: reset of the per-call words, trigger/compaction, deep, shallow + zero-fill
-        "gpu_launches": 4 * K,
+        # per step: reset of the per-call words, trigger/compaction, deep, the
+        # guard-band re-derivation (relaxed path), shallow + zero-fill
+        "gpu_launches": (5 if args.variant != 2 else 4) * K,
         "e2e": e2e,
         "feedback_loop": loop,
         "cpu_baseline": cpu,

@@ -116,7 +116,10 @@ typedef struct cvg_stats {
   int failure_kind;          /* CVG_FAIL_*                                    */
   int failing_kernel;        /* CVG_DEEP / CVG_SHALLOW, 0 when none          */
   double device_ms;          /* device time of the compute (CUDA events)      */
-  double h2d_ms, d2h_ms;     /* staging copies (host buffers only)           */
+  double h2d_ms, d2h_ms;     /* host-buffer calls with host inputs: staging
+                                copy time, summed over the pipeline's chunks
+                                (CUDA events; chunks overlap, so the sums can
+                                exceed device_ms); 0 otherwise               */
   long long h2d_bytes, d2h_bytes;
   long long n_recomputed;    /* deep levels whose relaxed stop decision fell
                                 in the guard band around newton_tol and were
@@ -130,6 +133,8 @@ typedef struct cvg_context cvg_context;
 
 const char* cvg_version(void);
 const char* cvg_last_error(void);
+/* The deep kernel (and its launch shape) of the context's last call. */
+const char* cvg_last_deep_kernel(const cvg_context* ctx);
 void cvg_default_options(cvg_options* opts);
 
 /* Creates a context on CUDA device `device` (requires compute capability 10.x). */
@@ -150,7 +155,12 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in,
  * capture: all pointers must be device memory; work is enqueued on `stream`
  * (a cudaStream_t, NULL = the context stream) and errors are latched on the
  * device.  cvg_convect_check() synchronises that stream, reads the latched
- * error, fills stats and clears it. */
+ * error of the last cvg_convect_async call and fills stats; the error is
+ * reported once (a second check without a new call returns CVG_OK with
+ * zeroed stats).  A call captured into a caller's CUDA graph uses the
+ * context workspace as sized by an earlier uncaptured call of at least the
+ * same column count (growth inside a capture returns CVG_ERR_INVALID); the
+ * workspace never shrinks or moves under such a graph. */
 cvg_status cvg_convect_async(cvg_context* ctx, const cvg_columns* in,
                              const cvg_options* opts, int kernel_mask,
                              const cvg_outputs* deep,

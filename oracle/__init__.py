@@ -250,6 +250,29 @@ def ref_make_grid(n, L=30, tropics_band=0.3, seed=42):
     return s, T, q
 
 
+def ref_run_parallel(kernel: str, s, T, q, opts: Options | None = None, n_threads=None, strategy=2, omp_chunk=1):
+    """The reference's run_parallel (sched.hpp:73-74) with its outputs:
+    (Result, wall seconds)."""
+    opts = opts or Options()
+    s, T, q = _soa(s, T, q)
+    L, n = T.shape
+    n_threads = n_threads or os.cpu_count() or 1
+    R = ref_lib()
+    h = R.ref_chunk_create(n, L, n, 0, s, T, q)
+    if not h:
+        raise RuntimeError("ref_chunk_create failed")
+    try:
+        r = Result(n, L)
+        w = C.c_double()
+        r.status = R.ref_run_parallel(h, 0 if kernel == "deep" else 1, opts.variant, opts.activity_threshold,
+                                      opts.newton_tol, opts.newton_max_iter, n_threads, strategy, omp_chunk,
+                                      C.byref(w), r.tend_T.ctypes.data, r.tend_q.ctypes.data, r.precip.ctypes.data,
+                                      r.work.ctypes.data, r.exited.ctypes.data)
+        return r, w.value
+    finally:
+        R.ref_chunk_free(h)
+
+
 def ref_time_run_parallel(s, T, q, opts: Options | None = None, n_threads=None,
                           strategy=2, omp_chunk=1, kernels=("deep", "shallow")):
     """Wall seconds of the reference run_parallel over the sample, one entry

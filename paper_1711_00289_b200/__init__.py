@@ -143,6 +143,9 @@ def load_library():
     vp, i64, i32, dbl = C.c_void_p, C.c_longlong, C.c_int, C.c_double
     L.cvg_version.restype = C.c_char_p
     L.cvg_last_error.restype = C.c_char_p
+    if hasattr(L, "cvg_last_deep_kernel"):
+        L.cvg_last_deep_kernel.restype = C.c_char_p
+        L.cvg_last_deep_kernel.argtypes = [vp]
     L.cvg_default_options.argtypes = [C.POINTER(KernelOptions)]
     L.cvg_context_create.argtypes = [i32, C.POINTER(vp)]
     L.cvg_context_free.argtypes = [vp]
@@ -356,15 +359,41 @@ class Context:
         """Enqueues on `stream` (a torch.cuda.Stream, raw handle or None for the
         context stream).  s/T/q and the output tuples are CUDA tensors
         (tend_T, tend_q, precip, work, exited)."""
+        import torch
         opts = opts or KernelOptions()
+        dev = torch.device("cuda", self.device)
+
+        def need(cond, what):
+            if not cond:
+                raise ValueError(f"convect_async: {what}")
+
+        def on_dev(t, dtype, name):
+            need(isinstance(t, torch.Tensor) and t.is_cuda and t.device == dev, f"{name} must be a tensor on {dev}")
+            need(t.dtype == dtype, f"{name} must be {dtype}")
+
         n = s.numel()
+        on_dev(s, torch.float64, "s")
+        need(s.dim() == 1 and s.stride(0) == 1, "s must be 1-D contiguous")
+        for name, t in (("T", T), ("q", q)):
+            on_dev(t, torch.float64, name)
+            need(t.dim() == 2 and t.shape[1] == n and t.stride(1) == 1, f"{name} must be [L][n] with unit column stride")
+        need(T.shape == q.shape and T.stride(0) == q.stride(0), "T and q must have the same shape and row pitch")
         L = T.shape[0]
         cols = _Columns(n, L, first_col, T.stride(0), s.data_ptr(), T.data_ptr(), q.data_ptr(), 1)
 
-        def outs(o):
+        def outs(o, name):
             if o is None:
                 return None
             tT, tq, pr, wk, ex = o
+            for nm, t in (("tend_T", tT), ("tend_q", tq)):
+                on_dev(t, torch.float64, f"{name}.{nm}")
+                need(t.dim() == 2 and tuple(t.shape) == (L, n) and t.stride(1) == 1,
+                     f"{name}.{nm} must be [L][n] with unit column stride")
+            need(tT.stride(0) == tq.stride(0), f"{name}: tend_T and tend_q must share a row pitch")
+            for nm, t, dt in (("precip", pr, torch.float64), ("work_units", wk, torch.int64),
+                              ("exited_early", ex, torch.uint8)):
+                on_dev(t, dt, f"{name}.{nm}")
+                need(t.dim() == 1 and t.numel() == n and t.stride(0) == 1, f"{name}.{nm} must be 1-D contiguous [n]")
             return C.byref(_Outputs(tT.data_ptr(), tq.data_ptr(), pr.data_ptr(), wk.data_ptr(),
                                     ex.data_ptr(), tT.stride(0), 1))
 
@@ -372,7 +401,8 @@ class Context:
         if stream is not None:
             h = getattr(stream, "cuda_stream", stream)
         rc = load_library().cvg_convect_async(self._h, C.byref(cols), C.byref(opts), kernels,
-                                              outs(deep), outs(shallow), h)
+                                              outs(deep, "deep") if kernels & DEEP else None,
+                                              outs(shallow, "shallow") if kernels & SHALLOW else None, h)
         _raise(rc)
 
     def profile_begin(self, max_steps: int):
@@ -384,6 +414,11 @@ class Context:
         n = C.c_int()
         _raise(load_library().cvg_profile_end(self._h, C.byref(n), buf.ctypes.data, capacity))
         return buf[: n.value].copy()
+
+    @property
+    def last_deep_kernel(self) -> str:
+        """The deep kernel (and launch shape) of this context's last call."""
+        return load_library().cvg_last_deep_kernel(self._h).decode()
 
     def fp64_peak_tflops(self, reps: int = 5) -> float:
         v = C.c_double()

@@ -110,6 +110,8 @@ struct Workspace {
   cudaStream_t stream = nullptr;  // chunk stream (host-buffer calls)
   cudaStream_t side = nullptr;    // shallow kernel, concurrent with deep
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_copy[4] = {};         // H2D start/end, D2H start/end of the slot's chunk
+  bool copy_timed = false;             // events recorded for the slot's current chunk
   DevBuf<long long> groups;            // compacted column groups with a triggered column
   DevBuf<int> counters;                // [0] listed groups, [1] triggered columns, [2] levels queued
                                        // for exact re-derivation, [3] columns rewritten by it
@@ -129,6 +131,7 @@ struct Workspace {
     CVG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     CVG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CVG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    for (cudaEvent_t& e : ev_copy) CVG_CUDA(cudaEventCreate(&e));
     counters.ensure(4);
     cursor.ensure(40);
     err.ensure(4);
@@ -145,6 +148,8 @@ struct Workspace {
     if (h_err) cudaFreeHost(h_err);
     if (h_count) cudaFreeHost(h_count);
     if (ev_fork) cudaEventDestroy(ev_fork);
+    for (cudaEvent_t& e : ev_copy)
+      if (e) cudaEventDestroy(e), e = nullptr;
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
@@ -242,6 +247,7 @@ struct cvg_context {
   DevBuf<unsigned> loop_flag;
   bool reset_kernel = true;   // CVG_RESET_KERNEL: one reset launch instead of three memsets
   std::vector<void*> retired;  // grown-out workspace buffers (graphs may reference them)
+  std::string last_deep_kernel;  // the deep kernel the last call launched (cvg_last_deep_kernel)
 };
 
 namespace {
@@ -355,6 +361,9 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
       else kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 4> : cvg::deep_tpc_kernel<VAR, 10, 96, 4>;
     }
     const int nwt = ov ? 12 : 10, blocks = ov ? 1 : 2;
+    ctx->last_deep_kernel = std::string("deep_tpc_kernel<lanes_per_column=") + std::to_string(tpc ? 1 : lpc_n) +
+                            ",k_order_precip=" + (tpc || !a.tree_precip ? "1" : "0") + ",warps=" +
+                            std::to_string(nwt) + ",blocks_per_sm=" + std::to_string(blocks) + ">";
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
     kern<<<ctx->num_sms * blocks, nwt * 32, smem, st>>>(a);
@@ -363,6 +372,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     // deep block size: kDeepWarpsOverlap leaves each SM room for three
     // shallow blocks beside the deep block; kDeepWarps when deep runs alone
     const int nw = ctx->deep_warps > 0 ? ctx->deep_warps : (ov ? cvg::kDeepWarpsOverlap : cvg::kDeepWarps);
+    ctx->last_deep_kernel = std::string("deep_kernel<warp_per_column,warps=") + std::to_string(nw) + ">";
     if (a.L <= 32) {
       if (nw == 16) launch_deep_t<VAR, true, 16>(ctx, a, st);
       else if (nw == 20) launch_deep_t<VAR, true, 20>(ctx, a, st);
@@ -628,6 +638,8 @@ const char* cvg_version(void) { return "0.3.0"; }
 
 const char* cvg_last_error(void) { return g_last_error.c_str(); }
 
+const char* cvg_last_deep_kernel(const cvg_context* ctx) { return ctx ? ctx->last_deep_kernel.c_str() : ""; }
+
 void cvg_default_options(cvg_options* o) {
   if (!o) return;
   o->variant = CVG_EXACT;
@@ -736,12 +748,30 @@ void launch_graph(cvg_context* ctx, const cvg_columns* in, const cvg_options* o,
     const unsigned char* b = static_cast<const unsigned char*>(p);
     key.insert(key.end(), b, b + n);
   };
-  const cvg_outputs none{};
-  put(in, sizeof(*in));
-  put(o, sizeof(*o));
+  // the key is built field by field (struct padding bytes of a caller's
+  // stack structs are indeterminate and must not defeat the cache)
+  auto put_cols = [&](const cvg_columns* c) {
+    put(&c->n_columns, sizeof(c->n_columns)); put(&c->n_levels, sizeof(c->n_levels));
+    put(&c->first_col, sizeof(c->first_col)); put(&c->ld, sizeof(c->ld)); put(&c->s, sizeof(c->s));
+    put(&c->T, sizeof(c->T)); put(&c->q, sizeof(c->q)); put(&c->on_device, sizeof(c->on_device));
+  };
+  auto put_opts = [&](const cvg_options* x) {
+    put(&x->variant, sizeof(x->variant)); put(&x->activity_threshold, sizeof(x->activity_threshold));
+    put(&x->newton_tol, sizeof(x->newton_tol)); put(&x->newton_max_iter, sizeof(x->newton_max_iter));
+    put(&x->flags, sizeof(x->flags));
+  };
+  auto put_outs = [&](const cvg_outputs* x) {
+    const cvg_outputs none{};
+    if (!x) x = &none;
+    put(&x->tend_T, sizeof(x->tend_T)); put(&x->tend_q, sizeof(x->tend_q)); put(&x->precip, sizeof(x->precip));
+    put(&x->work_units, sizeof(x->work_units)); put(&x->exited_early, sizeof(x->exited_early));
+    put(&x->ld, sizeof(x->ld)); put(&x->on_device, sizeof(x->on_device));
+  };
+  put_cols(in);
+  put_opts(o);
   put(&mask, sizeof(mask));
-  put((mask & CVG_DEEP) ? deep : &none, sizeof(none));
-  put((mask & CVG_SHALLOW) ? sh : &none, sizeof(none));
+  put_outs((mask & CVG_DEEP) ? deep : nullptr);
+  put_outs((mask & CVG_SHALLOW) ? sh : nullptr);
   put(&w.groups.p, sizeof(w.groups.p));
   put(&w.groups.cap, sizeof(w.groups.cap));
   put(&w.redo.p, sizeof(w.redo.p));
@@ -835,6 +865,7 @@ cvg_status cvg_convect_check(cvg_context* ctx, void* stream, cvg_stats* stats) {
         fclose(f);
       }
     }
+    ctx->pending = false;   // reported once; the next call resets the device words
     return collect(&w.h_err[0], &w.h_err[1], w.h_count[1], w.h_count[2], w.h_count[3], ctx->last_mask,
                    ctx->last_maxit, ctx->last_n, stats);
   });
@@ -881,14 +912,23 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
     CVG_CUDA(cudaEventRecord(ctx->ev_h0, ctx->stream));
     unsigned long long md = ~0ULL, ms_ = ~0ULL;
     long long trig = 0, recomp = 0, corr = 0;
+    double h2d_ms = 0.0, d2h_ms = 0.0;
     bool busy[kSlots] = {};
-    auto drain = [&](Workspace& w) {  // a slot's previous chunk: wait, fold its flags
+    auto drain = [&](Workspace& w) {  // a slot's previous chunk: wait, fold its flags and copy times
       CVG_CUDA(cudaStreamSynchronize(w.stream));
       md = std::min(md, w.h_err[0]);
       ms_ = std::min(ms_, w.h_err[1]);
       trig += w.h_count[1];
       recomp += w.h_count[2];
       corr += w.h_count[3];
+      if (w.copy_timed) {
+        float a = 0.f, b = 0.f;
+        CVG_CUDA(cudaEventElapsedTime(&a, w.ev_copy[0], w.ev_copy[1]));
+        CVG_CUDA(cudaEventElapsedTime(&b, w.ev_copy[2], w.ev_copy[3]));
+        h2d_ms += a;
+        d2h_ms += b;
+        w.copy_timed = false;
+      }
     };
     for (long long ci = 0; ci < nchunks; ++ci) {
       const int slot = (int)(ci % ctx->slots);
@@ -906,10 +946,12 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
         if (m > 0) { din.s = in->s + c0; din.T = in->T + c0; din.q = in->q + c0; }
       } else if (m > 0) {
         w.in_s.ensure(m); w.in_T.ensure(mL); w.in_q.ensure(mL);
+        CVG_CUDA(cudaEventRecord(w.ev_copy[0], w.stream));
         CVG_CUDA(cudaMemcpyAsync(w.in_s.p, in->s + c0, sizeof(double) * m, cudaMemcpyHostToDevice, w.stream));
         copy_rows_h2d(w.in_T.p, mp, in->T + c0, in->ld, m, L, w.stream);
         copy_rows_h2d(w.in_q.p, mp, in->q + c0, in->ld, m, L, w.stream);
         h2d += (long long)(sizeof(double) * (m + 2 * (size_t)m * L));
+        CVG_CUDA(cudaEventRecord(w.ev_copy[1], w.stream));
         din.s = w.in_s.p; din.T = w.in_T.p; din.q = w.in_q.p; din.ld = mp; din.on_device = 1;
       }
       auto stage = [&](const cvg_outputs* o, DevBuf<double>& T, DevBuf<double>& q, DevBuf<double>& p,
@@ -941,8 +983,14 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
         CVG_CUDA(cudaMemcpyAsync(o->exited_early + c0, d.exited_early, m, cudaMemcpyDeviceToHost, w.stream));
         d2h += (long long)(sizeof(double) * (2 * (size_t)m * L + m) + sizeof(long long) * m + m);
       };
+      const bool host_out = ((mask & CVG_DEEP) && !deep->on_device) || ((mask & CVG_SHALLOW) && !sh->on_device);
+      if (!in->on_device && host_out && m > 0) CVG_CUDA(cudaEventRecord(w.ev_copy[2], w.stream));
       if (mask & CVG_DEEP) unstage(deep, ddeep);
       if (mask & CVG_SHALLOW) unstage(sh, dsh);
+      if (!in->on_device && host_out && m > 0) {
+        CVG_CUDA(cudaEventRecord(w.ev_copy[3], w.stream));
+        w.copy_timed = true;
+      }
       read_flags_async(w, w.stream);
       busy[slot] = true;
     }
@@ -959,8 +1007,8 @@ cvg_status cvg_convect(cvg_context* ctx, const cvg_columns* in, const cvg_option
       float all = 0.f;
       CVG_CUDA(cudaEventElapsedTime(&all, ctx->ev_h0, ctx->ev_h1));
       stats->device_ms = all;   // whole call, transfers overlapped with compute
-      stats->h2d_ms = 0.0;
-      stats->d2h_ms = 0.0;
+      stats->h2d_ms = h2d_ms;   // summed over the chunks (each overlaps other chunks' work)
+      stats->d2h_ms = d2h_ms;
       stats->h2d_bytes = h2d;
       stats->d2h_bytes = d2h;
     }

@@ -25,7 +25,7 @@ BYTES_PER_COLUMN_30 = 1482.0
 # reference's calibrate(), hetero.cpp:110-163), refit whenever the kernels
 # change: a least-squares fit of the f02 step over its 4- and 8-way shares
 # (bench.py --slice R/W; split-column deep kernel at these sizes) gives
-# t = 19 us + 0.83 ns per triggered column + 0.23 ns per column -- a
+# t = 19 us + 0.83 ns per triggered column + 0.21 ns per column -- a
 # triggered column weighs ~4 plain columns.  (With the warp-per-column deep
 # kernel the ratio was 11: its deep-heavy shares ran their tail with few
 # warps; the split-column kernel's short claims removed that.)
@@ -83,24 +83,37 @@ def overlap_bounds(s, activity_threshold: float, world: int, L: int = 30) -> np.
     trig = np.concatenate([[0], np.cumsum(np.asarray(s) > activity_threshold)]).astype(np.int64)
     scale = L / 30.0
 
+    def cost(lo, e):
+        return scale * share_cost(trig[e] - trig[lo], e - lo)
+
+    def last_end(lo, target):
+        """Largest end e in [lo, n] with cost(lo, e) <= target (the cost of a
+        range grows with its end): bisection, O(log n) evaluations."""
+        a, b = lo, n
+        if cost(lo, n) <= target:
+            return n
+        while b - a > 1:
+            mid = (a + b) // 2
+            if cost(lo, mid) <= target:
+                a = mid
+            else:
+                b = mid
+        return a
+
     def greedy(target):
         b = [0]
         for _ in range(world - 1):
-            lo = b[-1]
-            ends = np.arange(lo, n + 1)
-            c = scale * share_cost(trig[ends] - trig[lo], ends - lo)
-            k = int(np.searchsorted(c > target, True))   # first end over the target
-            b.append(lo + max(k - 1, 0))
+            b.append(last_end(b[-1], target))
         b.append(n)
         return np.array(b, dtype=np.int64)
 
     def worst(b):
-        return max(scale * share_cost(trig[b[i + 1]] - trig[b[i]], b[i + 1] - b[i]) for i in range(world))
+        return max(cost(b[i], b[i + 1]) for i in range(world))
 
-    lo_t, hi_t = 0.0, float(scale * share_cost(trig[n], n))
+    lo_t, hi_t = 0.0, float(cost(0, n))
     for _ in range(40):
         mid = 0.5 * (lo_t + hi_t)
-        if worst(greedy(mid)) <= mid + 1e-12 and greedy(mid)[-2] <= n:
+        if worst(greedy(mid)) <= mid + 1e-12:
             hi_t = mid
         else:
             lo_t = mid

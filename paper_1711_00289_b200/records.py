@@ -98,6 +98,15 @@ def run_gpu_record(line: dict, rep: int = 0) -> BenchRecord:
         notes.insert(1, f"roofline_frac={fmt(frac)}")
     if e2e:
         notes.append(f"e2e_cols_per_s={fmt(e2e['value'])}")
+    par = line.get("parity") or {}
+    # flagged_cols: columns exempted from the parity rule;
+    # rederived: guard-band levels re-derived exactly; rewritten: count fixes
+    notes.append(f"flagged_cols={int(par.get('exempt_columns', 0))}")
+    if "rederived_levels" in par:
+        notes.append(f"rederived={int(par['rederived_levels'])}")
+        notes.append(f"rewritten={int(par['rewritten_patches'])}")
+    if "work_mismatch" in par:
+        notes.append(f"parity_ok={int(bool(par.get('ok')))}")
     return BenchRecord("run-gpu", config_hash(line["config"]), rep, dev_s, 0.0, line.get("imbalance", 0.0), 0.0,
                        max(e2e_s - dev_s, 0.0) if e2e else 0.0, ";".join(notes))
 

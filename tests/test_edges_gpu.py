@@ -362,3 +362,84 @@ def test_async_call_inside_a_caller_graph(ctx):
     torch.cuda.synchronize()
     both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in do]), O.convection("deep", s, T, q))
     both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in so]), O.convection("shallow", s, T, q))
+
+
+def test_async_argument_validation(ctx):
+    """convect_async checks devices, dtypes, shapes and strides before the
+    kernels see a pointer (a wrong pitch would read out of bounds)."""
+    import torch
+    dev = torch.device("cuda", 0)
+    s, T, q = G.make_config("c1", n=256, seed=3)
+    L, n = T.shape
+    ds, dT, dq = (torch.from_numpy(a).to(dev) for a in (s, T, q))
+
+    def outs(dt=torch.float64):
+        return (torch.empty((L, n), dtype=dt, device=dev), torch.empty((L, n), dtype=torch.float64, device=dev),
+                torch.empty(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.int64, device=dev),
+                torch.empty(n, dtype=torch.uint8, device=dev))
+    do, so = outs(), outs()
+    bad_cases = [
+        (ds.cpu(), dT, dq, do, so),                               # host tensor
+        (ds.float(), dT, dq, do, so),                             # dtype
+        (ds, dT.t().contiguous().t(), dq, do, so),                # column stride != 1
+        (ds, dT, torch.empty((L, 2 * n), dtype=torch.float64, device=dev)[:, :n], do, so),   # q pitch != T pitch
+        (ds, dT, dq, outs(torch.float32), so),                    # output dtype
+        (ds, dT, dq, do, so[:4] + (torch.empty(n, dtype=torch.int8, device=dev),)),          # exited dtype
+    ]
+    for args in bad_cases:
+        with pytest.raises(ValueError):
+            ctx.convect_async(*args)
+    ctx.convect_async(ds, dT, dq, do, so)
+    ctx.check()
+
+
+def test_check_reports_a_failure_once(ctx):
+    import torch
+    dev = torch.device("cuda", 0)
+    s, T, q = G.make_config("c1", n=512, seed=8)
+    L, n = T.shape
+    ds, dT, dq = (torch.from_numpy(a).to(dev) for a in (s, T, q))
+    outs = lambda: (torch.empty((L, n), dtype=torch.float64, device=dev),   # noqa: E731
+                    torch.empty((L, n), dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.float64, device=dev),
+                    torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.uint8, device=dev))
+    ds[40] = float("inf")
+    ctx.convect_async(ds, dT, dq, outs(), outs())
+    with pytest.raises(P.KernelError) as e:
+        ctx.check()
+    assert e.value.column == 40
+    st = ctx.check()   # reported once
+    assert st.failing_column == 0 and st.n_columns == 0
+
+
+def test_capture_refuses_workspace_growth():
+    """A call captured into a caller's graph must not allocate: on a fresh
+    context the first (larger) call inside a capture is refused with
+    CVG_ERR_INVALID, and the context keeps working."""
+    import torch
+    from conftest import env_context
+    c = env_context(CVG_GRAPH="1")
+    dev = torch.device("cuda", 0)
+    s, T, q = G.make_config("c2", n=8192, seed=12)
+    L, n = T.shape
+    ds, dT, dq = (torch.from_numpy(a).to(dev) for a in (s, T, q))
+    outs = lambda: (torch.zeros((L, n), dtype=torch.float64, device=dev),   # noqa: E731
+                    torch.zeros((L, n), dtype=torch.float64, device=dev), torch.zeros(n, dtype=torch.float64, device=dev),
+                    torch.zeros(n, dtype=torch.int64, device=dev), torch.zeros(n, dtype=torch.uint8, device=dev))
+    do, so = outs(), outs()
+    st = torch.cuda.Stream()
+    refused = False
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            try:
+                c.convect_async(ds, dT, dq, do, so, stream=st)
+            except ValueError as e:
+                refused = "capture" in str(e)
+    except RuntimeError:
+        pass   # torch may reject the empty capture
+    assert refused
+    torch.cuda.synchronize()
+    c.convect_async(ds, dT, dq, do, so, stream=st)   # uncaptured: sizes the workspace
+    c.check(st)
+    both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in do]), O.convection("deep", s, T, q))
+    c.close()

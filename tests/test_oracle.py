@@ -265,3 +265,17 @@ def test_exp_restatement_bit_exact_against_libm():
     a, b = O.exp_gl(x), O.libm_exp(x)
     same = (a.view(np.int64) == b.view(np.int64)) | (np.isnan(a) & np.isnan(b))
     assert same.all(), f"{int((~same).sum())} of {x.size} differ, e.g. x={x[~same][:4]}"
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_reference_run_parallel_outputs_equal_oracle():
+    """The reference's threaded run_parallel (the CPU baseline bench.py times
+    and checks the GPU against) returns the serial oracle's outputs bit for
+    bit (sched.cpp:145: disjoint output slots)."""
+    s, T, q = G.make_config("c2", n=3000, seed=17)
+    for kernel in ("deep", "shallow"):
+        r, wall = O.ref_run_parallel(kernel, s, T, q, n_threads=4)
+        o = O.convection(kernel, s, T, q)
+        assert r.status == 0 and wall > 0.0
+        for f in FIELDS:
+            assert bits_equal(getattr(r, f), getattr(o, f)), (kernel, f)

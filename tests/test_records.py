@@ -10,7 +10,9 @@ LINE = {"metric": "convective columns/sec (deep+shallow, fp64)", "value": 139671
         "ms_per_step": 0.6334425735473633, "config": {"workload": "c4", "n_columns": 884736, "levels": 30,
                                                        "variant": 0},
         "step_roofline": {"frac": 0.44844353932638426},
-        "e2e": {"value": 47987623.5, "ms_per_step": 18.43675380005152}}
+        "e2e": {"value": 47987623.5, "ms_per_step": 18.43675380005152},
+        "parity": {"ok": True, "exempt_columns": 0, "work_mismatch": 0, "rederived_levels": 12509,
+                   "rewritten_patches": 77}}
 
 
 def test_header_is_the_reference_schema():
@@ -36,6 +38,7 @@ def test_run_gpu_record_roundtrips_through_the_reference():
     back = R.records_from_csv(csv)
     assert back[0].experiment == "run-gpu" and back[1].rep == 1
     assert "cols_per_s=" in back[0].notes and "roofline_frac=" in back[0].notes and "," not in back[0].notes
+    assert "flagged_cols=0" in back[0].notes and "rederived=12509" in back[0].notes and "parity_ok=1" in back[0].notes
     assert abs(back[0].wall_s - LINE["ms_per_step"] * 1e-3) < 1e-15
     if O.ref_available():
         st, n, text = O.ref_records_roundtrip(csv)
