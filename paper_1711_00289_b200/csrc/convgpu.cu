@@ -348,7 +348,13 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     // beside the shallow kernel: one 12-warp block per SM (registers capped
     // so three shallow blocks fit); alone: two 10-warp blocks per SM
     void (*kern)(cvg::DeepArgs) = nullptr;
-    if (tpc) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
+    if (fused) {   // feedback loop (the deep kernel runs alone): the state-advancing builds
+      if (tpc) kern = cvg::deep_tpc_kernel<VAR, 10, 96, 1, true, true>;
+      else if (a.tree_precip) kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 10, 96, 2, false, true>
+                                                : cvg::deep_tpc_kernel<VAR, 10, 96, 4, false, true>;
+      else kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 10, 96, 2, true, true>
+                             : cvg::deep_tpc_kernel<VAR, 10, 96, 4, true, true>;
+    } else if (tpc) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
     // the split kernels are capped at 80 registers beside the shallow kernel
     // (79 used, no spills): room for a fourth shallow block per SM, which
     // the shallow kernel -- the step's tail -- turns into speed (f02 0.435
@@ -401,7 +407,9 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     const unsigned blocks = (unsigned)((b.n + cvg::kShallowThreads - 1) / cvg::kShallowThreads);
     const bool relax = VAR != cvg::kVarApprox && !strict;
     void (*k)(cvg::ShallowArgs) = nullptr;
-    if (sh && relax) {
+    if (sh && fused) {   // feedback loop: the state-advancing builds
+      k = relax ? cvg::shallow_kernel<VAR, true, false, true, 8, true> : cvg::shallow_kernel<VAR, true, false, false, 8, true>;
+    } else if (sh && relax) {
       if (dp && ctx->shallow_minb == 12) k = cvg::shallow_kernel<VAR, true, true, true, 12>;
       else if (dp && ctx->shallow_minb == 16) k = cvg::shallow_kernel<VAR, true, true, true, 16>;
       else if (dp) k = cvg::shallow_kernel<VAR, true, true, true>;
