@@ -216,6 +216,7 @@ struct cvg_context {
   // rounding noise of tol)
   double guard = 1.0 / 128;
   bool redo_launch = true;  // CVG_REDO=0: skip the re-derivation kernel (timing experiments only)
+  bool redo_inline = false; // CVG_REDO_INLINE: re-derive flagged solves inside the deep kernel
   long long chunk_cols = kChunkCols;  // CVG_CHUNK_COLS: host-call pipeline chunk
   int slots = 3;                      // CVG_SLOTS: workspaces used by host-buffer calls (1..kSlots)
   const char* trace_path = nullptr;   // CVG_TRACE: per-block (kernel, smid, start, end)
@@ -239,6 +240,7 @@ struct cvg_context {
   bool use_graphs = true;
   int deep_lpc = -1;          // CVG_DEEP_LPC: lanes per column for calls under kTpcMinColumns (-1 by size, 0 off, 2, 4)
   int deep_tpc = 2;           // CVG_DEEP_TPC: thread-per-column deep kernel: 0 never, 1 always, 2 for large calls
+  int deep_alone = 1;         // CVG_DEEP_ALONE: deep-only launches as 2 x 16 warps x 64 registers (1) or 2 x 10 x 96 (0)
   // cvg_timestep state, kept across calls (the reference's persistent
   // buffers, hetero.hpp:44)
   LoopBufs loop;
@@ -338,35 +340,61 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // thread per column, CVG_DEEP_LPC=0 the warp-per-column kernel,
   // CVG_DEEP_LPC=2/4 the split width.
   const bool tpc_forced = ctx->deep_tpc == 1;
-  int lpc_n = ctx->deep_lpc >= 0 ? ctx->deep_lpc : (a.n >= cvg::kTpcMinColumns / 2 ? 2 : 4);
+  // lanes per column by call size: 2 for large calls, 4 below 160k columns,
+  // 8 below 100k (shorter per-warp chains when a call holds too few columns
+  // to keep 2368 warps busy: 8-way f02 shares 0.089 -> 0.084 ms)
+  int lpc_n = ctx->deep_lpc >= 0 ? ctx->deep_lpc
+                                 : (a.n >= cvg::kTpcMinColumns / 2 ? 2 : a.n >= 100000 ? 4 : 8);
+  if (lpc_n == 8 && (fused || !a.tree_precip || !ov)) lpc_n = 4;   // 8 lanes: overlapped relaxed builds only
   if (fused && lpc_n <= 1 && !tpc_forced) lpc_n = 2;   // the warp-per-column kernel has no feedback-loop mode
   const bool lpc = !tpc_forced && dp && lpc_n > 1;
   const bool tpc = !lpc && dp && a.L <= 32 &&
                    (tpc_forced || (ctx->deep_tpc == 2 && a.n >= cvg::kTpcMinColumns));
   if (tpc || lpc) {
     const size_t smem = cvg::deep_table_bytes();
-    // beside the shallow kernel: one 12-warp block per SM (registers capped
-    // so three shallow blocks fit); alone: two 10-warp blocks per SM
+    // Launch shapes (warps per block x register cap, blocks per SM).  Beside
+    // the shallow kernel: one 16-warp block capped at 64 registers (no
+    // spills) -- exactly the register file left by four 128-thread shallow
+    // blocks (f02 step 0.459 -> 0.429 ms against 12 warps x 80 registers;
+    // 18 x 56 and 20 x 48 spill and lose).  Alone (deep only, the feedback
+    // loop): two blocks per SM, 16 x 64 (default; f02 deep 0.292 ms against
+    // 0.308 at 10 x 96, CVG_DEEP_ALONE=0).
+    // The one-thread-per-column kernel (CVG_DEEP_TPC=1) keeps 12 x 104.
     void (*kern)(cvg::DeepArgs) = nullptr;
+    const bool wide = ctx->deep_alone == 1;   // alone: 2 x 16 x 64 instead of 2 x 10 x 96
+    int nwt = 0;
+    const int blocks = ov ? 1 : 2;
     if (fused) {   // feedback loop (the deep kernel runs alone): the state-advancing builds
-      if (tpc) kern = cvg::deep_tpc_kernel<VAR, 10, 96, 1, true, true>;
-      else if (a.tree_precip) kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 10, 96, 2, false, true>
-                                                : cvg::deep_tpc_kernel<VAR, 10, 96, 4, false, true>;
-      else kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 10, 96, 2, true, true>
-                             : cvg::deep_tpc_kernel<VAR, 10, 96, 4, true, true>;
-    } else if (tpc) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
-    // the split kernels are capped at 80 registers beside the shallow kernel
-    // (79 used, no spills): room for a fourth shallow block per SM, which
-    // the shallow kernel -- the step's tail -- turns into speed (f02 0.435
-    // -> 0.420 ms; 8-way max share 0.078 -> 0.072 ms)
-    else if (a.tree_precip) {
-      if (lpc_n == 2) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 2, false> : cvg::deep_tpc_kernel<VAR, 10, 96, 2, false>;
-      else kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 4, false> : cvg::deep_tpc_kernel<VAR, 10, 96, 4, false>;
+      nwt = wide ? 16 : 10;
+      if (tpc) nwt = 10, kern = cvg::deep_tpc_kernel<VAR, 10, 96, 1, true, true>;
+      else if (a.tree_precip)
+        kern = wide ? (lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 16, 64, 2, false, true>
+                                  : cvg::deep_tpc_kernel<VAR, 16, 64, 4, false, true>)
+                    : (lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 10, 96, 2, false, true>
+                                  : cvg::deep_tpc_kernel<VAR, 10, 96, 4, false, true>);
+      else
+        kern = wide ? (lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 16, 64, 2, true, true>
+                                  : cvg::deep_tpc_kernel<VAR, 16, 64, 4, true, true>)
+                    : (lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 10, 96, 2, true, true>
+                                  : cvg::deep_tpc_kernel<VAR, 10, 96, 4, true, true>);
+    } else if (tpc) {
+      nwt = ov ? 12 : 10;
+      kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
+    } else if (ov) {
+      nwt = 16;
+      if (a.tree_precip)
+        kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 16, 64, 2, false>
+               : lpc_n == 8 ? cvg::deep_tpc_kernel<VAR, 16, 64, 8, false> : cvg::deep_tpc_kernel<VAR, 16, 64, 4, false>;
+      else kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 16, 64, 2> : cvg::deep_tpc_kernel<VAR, 16, 64, 4>;
+    } else if (wide) {
+      nwt = 16;
+      if (a.tree_precip) kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 16, 64, 2, false> : cvg::deep_tpc_kernel<VAR, 16, 64, 4, false>;
+      else kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 16, 64, 2> : cvg::deep_tpc_kernel<VAR, 16, 64, 4>;
     } else {
-      if (lpc_n == 2) kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 2> : cvg::deep_tpc_kernel<VAR, 10, 96, 2>;
-      else kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 80, 4> : cvg::deep_tpc_kernel<VAR, 10, 96, 4>;
+      nwt = 10;
+      if (a.tree_precip) kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 10, 96, 2, false> : cvg::deep_tpc_kernel<VAR, 10, 96, 4, false>;
+      else kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, 10, 96, 2> : cvg::deep_tpc_kernel<VAR, 10, 96, 4>;
     }
-    const int nwt = ov ? 12 : 10, blocks = ov ? 1 : 2;
     ctx->last_deep_kernel = std::string("deep_tpc_kernel<lanes_per_column=") + std::to_string(tpc ? 1 : lpc_n) +
                             ",k_order_precip=" + (tpc || !a.tree_precip ? "1" : "0") + ",warps=" +
                             std::to_string(nwt) + ",blocks_per_sm=" + std::to_string(blocks) + ">";
@@ -390,7 +418,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
       else launch_deep_t<VAR, false, 12>(ctx, a, st);
     }
   }
-  if (dp && a.relaxed && VAR != cvg::kVarApprox && ctx->redo_launch) {
+  if (dp && a.relaxed && VAR != cvg::kVarApprox && ctx->redo_launch && !a.inline_redo) {
     // exact re-derivation of the solves the guard band flagged (a few
     // microseconds: one exact solve per thread, patches by the last block)
     const size_t smem = std::max((size_t)(cvg::kRedoThreads / 32) * a.L * sizeof(double),
@@ -494,6 +522,7 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.fix = w.fix.p;
     a.blocks_done = reinterpret_cast<unsigned*>(w.cursor.p + 16);   // reset per call
     a.redo_cap = (int)cap;
+    a.inline_redo = ctx->redo_inline;
     a.redo_count = w.counters.p + 2;
     a.fix_count = w.counters.p + 3;
     a.L = L;
@@ -682,11 +711,13 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_GRAPH")) ctx->use_graphs = atoi(e) != 0;
     if (const char* e = getenv("CVG_DEEP_TPC")) ctx->deep_tpc = atoi(e);
     if (const char* e = getenv("CVG_DEEP_LPC")) ctx->deep_lpc = atoi(e);
+    if (const char* e = getenv("CVG_DEEP_ALONE")) ctx->deep_alone = atoi(e);
     if (const char* e = getenv("CVG_RESET_KERNEL")) ctx->reset_kernel = atoi(e) != 0;
     if (const char* e = getenv("CVG_CARVEOUT")) ctx->carveout = atoi(e);
     if (const char* e = getenv("CVG_FAR32")) ctx->far32 = atoi(e) != 0;
     if (const char* e = getenv("CVG_GUARD")) ctx->guard = std::max(0.0, std::min(0.5, atof(e)));
     if (const char* e = getenv("CVG_REDO")) ctx->redo_launch = atoi(e) != 0;
+    if (const char* e = getenv("CVG_REDO_INLINE")) ctx->redo_inline = atoi(e) != 0;
     if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
     if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
