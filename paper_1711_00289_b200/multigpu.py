@@ -23,14 +23,12 @@ BYTES_PER_COLUMN_30 = 1482.0
 
 # Measured per-unit step times on one B200 at L = 30 (the analogue of the
 # reference's calibrate(), hetero.cpp:110-163), refit whenever the kernels
-# change: a least-squares fit of the f02 step over its 4- and 8-way shares
-# (bench.py --slice R/W; split-column deep kernel at these sizes) gives
-# t = 19 us + 0.83 ns per triggered column + 0.21 ns per column -- a
-# triggered column weighs ~4 plain columns.  (With the warp-per-column deep
-# kernel the ratio was 11: its deep-heavy shares ran their tail with few
-# warps; the split-column kernel's short claims removed that.)
-MEASURED_NS_PER_TRIGGERED = 0.83
-MEASURED_NS_PER_COLUMN = 0.21
+# change (tools/fit_partition.py: c4, c5_50 and c5_05 ranges of 1/2/4/8-way
+# balanced and naive splits, each a whole step, least squares): t = 30 us +
+# 0.92 ns per triggered column + 0.165 ns per column -- a triggered column
+# weighs ~5.6 plain columns (profiles/r03_fit_partition.json).
+MEASURED_NS_PER_TRIGGERED = 0.92
+MEASURED_NS_PER_COLUMN = 0.165
 
 
 def partition_weights(L: int = 30, hbm_gbs: float = 6558.7, fp64_tflops: float = 34.0, mode: str = "balanced"):

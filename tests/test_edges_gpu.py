@@ -443,3 +443,68 @@ def test_capture_refuses_workspace_growth():
     c.check(st)
     both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in do]), O.convection("deep", s, T, q))
     c.close()
+
+
+@pytest.mark.parametrize("env", [{}, {"CVG_DEEP_LPC": "8"}, {"CVG_DEEP_TPC": "1"}, {"CVG_DEEP_LPC": "0", "CVG_DEEP_TPC": "0"},
+                                 {"CVG_REDO_INLINE": "1"}, {"CVG_OVERLAP": "0"}],
+                         ids=["default", "lpc8", "tpc", "warp", "inline_redo", "serial"])
+@pytest.mark.parametrize("variant,strict", [(0, False), (1, False), (2, False), (0, True)])
+def test_writes_stay_in_bounds_and_cover_outputs(env, variant, strict):
+    """Canary check (compute-sanitizer is unavailable on this pool): every
+    buffer sits inside a larger allocation filled with a sentinel -- a row
+    pitch wider than n and guard rows / elements on both sides.  After the
+    call the inputs are bit-identical, every output element inside the
+    region was written (no sentinel left), and nothing outside it changed."""
+    import torch
+    from conftest import env_context
+    c = env_context(**env)
+    dev = torch.device("cuda", 0)
+    n, L, pad = 1000 + 37, 30, 24          # ragged n (last group partial), pitch n + pad
+    s, T, q = G.make_config("c1", n=n, seed=44)
+    ld = n + pad
+    SENT = float.fromhex("0x1.dead0beefp+1000")
+
+    def rows(x=None):
+        base = torch.full((L + 2, ld), SENT, dtype=torch.float64, device=dev)
+        if x is not None:
+            base[1:L + 1, :n] = torch.from_numpy(x)
+        return base, base[1:L + 1, :n]
+
+    def vec(dtype, x=None, fill=SENT):
+        base = torch.full((n + 2 * pad,), fill, dtype=dtype, device=dev) if dtype == torch.float64 else \
+            torch.full((n + 2 * pad,), 123, dtype=dtype, device=dev)
+        if x is not None:
+            base[pad:pad + n] = torch.from_numpy(x)
+        return base, base[pad:pad + n]
+
+    sb, sv = vec(torch.float64, s)
+    Tb, Tv = rows(T)
+    qb, qv = rows(q)
+    ins = [t.clone() for t in (sb, Tb, qb)]
+    bufs, outs = [], []
+    for _ in range(2):
+        tTb, tTv = rows()
+        tqb, tqv = rows()
+        pb, pv = vec(torch.float64)
+        wb, wv = vec(torch.int64)
+        xb, xv = vec(torch.uint8)
+        bufs.append((tTb, tqb, pb, wb, xb))
+        outs.append((tTv, tqv, pv, wv, xv))
+    o = P.KernelOptions(variant=variant, strict=strict)
+    c.convect_async(sv, Tv, qv, outs[0], outs[1], o)
+    c.check()
+    for a, b in zip(ins, (sb, Tb, qb)):
+        assert torch.equal(a.view(torch.int64) if a.dtype == torch.float64 else a,
+                           b.view(torch.int64) if b.dtype == torch.float64 else b), "an input was modified"
+    for (tTb, tqb, pb, wb, xb), (tTv, tqv, pv, wv, xv) in zip(bufs, outs):
+        for b, v in ((tTb, tTv), (tqb, tqv)):
+            assert not (v == SENT).any(), "an output element was not written"
+            mask = torch.ones_like(b, dtype=torch.bool)
+            mask[1:L + 1, :n] = False
+            assert (b[mask] == SENT).all(), "a write outside the [L][n] region (pitch gap or guard rows)"
+        assert not (pv == SENT).any() and (pb[:pad] == SENT).all() and (pb[pad + n:] == SENT).all()
+        for b in (wb, xb):
+            assert (b[:pad] == 123).all() and (b[pad + n:] == 123).all(), "a write before / after a vector"
+    od = O.convection("deep", s, T, q, O.Options(variant=variant))
+    assert np.array_equal(outs[0][3].cpu().numpy(), od.work)
+    c.close()
