@@ -1,9 +1,6 @@
-// bulkcopy.cuh -- sm_90+/sm_100a bulk-copy (TMA engine) and mbarrier helpers.
-//
-// cp.async.bulk moves a contiguous global range into shared memory on the
-// SM's TMA unit and signals completion on an mbarrier transaction count, so
-// a streaming kernel keeps whole tiles in flight without holding them in
-// registers.
+// bulkcopy.cuh -- small PTX helpers of the deep kernels: shared-memory
+// addresses, the warp-per-column kernel's cp.async group-entry prefetch, and
+// the 256-bit global store of a 4-column group row.
 #pragma once
 #include <cstdint>
 
@@ -13,67 +10,15 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-// Arrive (count 1) and add `bytes` to the barrier's expected transaction count.
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// Global -> shared bulk copy of `bytes` (multiple of 16, both addresses
-// 16-byte aligned), completing on `bar`.
-__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst_smem)),
-      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// L2 prefetch of a contiguous global range on the TMA engine (no
-// registers, no shared memory, no completion tracking); bytes % 16 == 0.
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
-}
-
-// Per-thread asynchronous global -> shared copies (LDGSTS): the data lands
-// in shared memory without occupying registers or a register scoreboard;
-// the issuing thread waits for its own copies with cp_async_wait_all.
-__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src_gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async8_u32(unsigned dst_smem, const void* src_gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst_smem), "l"(src_gmem) : "memory");
-}
-__device__ __forceinline__ double lds_f64(unsigned addr) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-  return v;
-}
 // A shared-memory address the compiler cannot rematerialise (it would
 // otherwise recompute it from %cgactaid inside loops under register caps).
 __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
   asm volatile("mov.b32 %0, %0;" : "+r"(x));
   return x;
+}
+// 8-byte cp.async global -> shared (dst as a shared-window address).
+__device__ __forceinline__ void cp_async8_u32(unsigned dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst_smem), "l"(src_gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }

@@ -81,11 +81,22 @@ open(os.path.join(prof, f"{tag}_ncu_summary.md"), "w").write("\n".join(lines) + 
 deep = [d for d in caps if "deep_kernel" in d["kernel"] or "deep_tpc_kernel" in d["kernel"]]
 if deep:
     d = deep[0]
-    rd = float(d["dram__bytes_read.sum"].split()[0]); wr = float(d["dram__bytes_write.sum"].split()[0])
-    unit = d["dram__bytes_read.sum"].split()[1] if len(d["dram__bytes_read.sum"].split()) > 1 else "byte"
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-    json.dump({"config": config, "tag": tag, "kernel": d["kernel"],
-               "dram_bytes_per_launch": (rd + wr) * scale,
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def val(k):
+        f = d[k].split()
+        return float(f[0]) * scale.get(f[1] if len(f) > 1 else "byte", 1)
+    # the library's own name for the launch (cvg_last_deep_kernel), from the
+    # template arguments <VAR, warps, regcap, lanes per column, k-order, fused>
+    # and the grid (blocks per SM over 148 SMs)
+    desc = None
+    m = __import__("re").search(r"deep_tpc_kernel<(\d+), (\d+), (\d+), (\d+), (\d+)", d["kernel"])
+    if m:
+        grid = int(float(d.get("launch__grid_size", "148").split()[0]))
+        desc = (f"deep_tpc_kernel<lanes_per_column={m.group(4)},k_order_precip={m.group(5)},warps={m.group(2)},"
+                f"blocks_per_sm={max(1, grid // 148)}>")
+    json.dump({"config": config, "tag": tag, "kernel": d["kernel"], "kernel_desc": desc,
+               "dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
                "source": f"profiles/{tag}_ncu_summary.md (ncu --set full, one launch)"},
               open(os.path.join(prof, "deep_traffic.json"), "w"), indent=1)
 print("\n".join(lines))
