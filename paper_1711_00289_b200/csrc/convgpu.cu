@@ -216,7 +216,7 @@ struct cvg_context {
   // rounding noise of tol)
   double guard = 1.0 / 128;
   bool redo_launch = true;  // CVG_REDO=0: skip the re-derivation kernel (timing experiments only)
-  bool redo_inline = false; // CVG_REDO_INLINE: re-derive flagged solves inside the deep kernel
+  int redo_inline = -1;     // CVG_REDO_INLINE: re-derive flagged solves inside the deep kernel (1), with redo_kernel (0), by size (-1)
   long long chunk_cols = kChunkCols;  // CVG_CHUNK_COLS: host-call pipeline chunk
   int slots = 3;                      // CVG_SLOTS: workspaces used by host-buffer calls (1..kSlots)
   const char* trace_path = nullptr;   // CVG_TRACE: per-block (kernel, smid, start, end)
@@ -522,7 +522,10 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     a.fix = w.fix.p;
     a.blocks_done = reinterpret_cast<unsigned*>(w.cursor.p + 16);   // reset per call
     a.redo_cap = (int)cap;
-    a.inline_redo = ctx->redo_inline;
+    // small calls re-derive inline (no dependent redo launch on a short
+    // critical path: 8-way f02 shares 0.083 -> 0.079 ms); large calls hide
+    // redo_kernel beside the shallow kernel's tail (inline costs 1-2 % there)
+    a.inline_redo = ctx->redo_inline > 0 || (ctx->redo_inline < 0 && n < 100000);
     a.redo_count = w.counters.p + 2;
     a.fix_count = w.counters.p + 3;
     a.L = L;
@@ -717,7 +720,7 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_FAR32")) ctx->far32 = atoi(e) != 0;
     if (const char* e = getenv("CVG_GUARD")) ctx->guard = std::max(0.0, std::min(0.5, atof(e)));
     if (const char* e = getenv("CVG_REDO")) ctx->redo_launch = atoi(e) != 0;
-    if (const char* e = getenv("CVG_REDO_INLINE")) ctx->redo_inline = atoi(e) != 0;
+    if (const char* e = getenv("CVG_REDO_INLINE")) ctx->redo_inline = atoi(e);
     if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
     if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
