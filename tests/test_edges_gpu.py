@@ -445,9 +445,9 @@ def test_capture_refuses_workspace_growth():
     c.close()
 
 
-@pytest.mark.parametrize("env", [{}, {"CVG_DEEP_LPC": "8"}, {"CVG_DEEP_TPC": "1"}, {"CVG_DEEP_LPC": "0", "CVG_DEEP_TPC": "0"},
-                                 {"CVG_REDO_INLINE": "1"}, {"CVG_OVERLAP": "0"}],
-                         ids=["default", "lpc8", "tpc", "warp", "inline_redo", "serial"])
+@pytest.mark.parametrize("env", [{}, {"CVG_DEEP_LPC": "2"}, {"CVG_DEEP_TPC": "1"}, {"CVG_DEEP_LPC": "0", "CVG_DEEP_TPC": "0"},
+                                 {"CVG_REDO_INLINE": "0"}, {"CVG_OVERLAP": "0"}],
+                         ids=["default", "lpc2", "tpc", "warp", "redo_kernel", "serial"])
 @pytest.mark.parametrize("variant,strict", [(0, False), (1, False), (2, False), (0, True)])
 def test_writes_stay_in_bounds_and_cover_outputs(env, variant, strict):
     """Canary check (compute-sanitizer is unavailable on this pool): every

@@ -333,14 +333,17 @@ def test_full_grid_variants_and_strict(ctx, variant, strict):
         assert np.array_equal(pick.precip.view(np.int64), od.precip.view(np.int64))
 
 
-@pytest.fixture(scope="module", params=[("0", "0"), ("0", "2")], ids=["warp_per_column", "lpc2"])
+@pytest.fixture(scope="module", params=[("0", "0", "-1"), ("0", "2", "-1"), ("0", "4", "0")],
+                ids=["warp_per_column", "lpc2", "lpc4_redo_kernel"])
 def kernel_ctx(request):
-    """Deep kernels the size switch does not pick at test sizes: the
-    warp-per-column kernel on the relaxed path (CVG_DEEP_LPC=0) and the
-    2-lanes-per-column split (CVG_DEEP_LPC=2)."""
+    """Deep kernels / re-derivation paths the size switches do not pick at
+    test sizes: the warp-per-column kernel on the relaxed path
+    (CVG_DEEP_LPC=0), the 2- and 4-lanes-per-column splits, and the separate
+    redo_kernel (CVG_REDO_INLINE=0; calls below 100k columns re-derive
+    inline by default)."""
     from conftest import env_context
-    tpc, lpc = request.param
-    c = env_context(CVG_DEEP_TPC=tpc, CVG_DEEP_LPC=lpc)
+    tpc, lpc, inline = request.param
+    c = env_context(CVG_DEEP_TPC=tpc, CVG_DEEP_LPC=lpc, CVG_REDO_INLINE=inline)
     yield c
     c.close()
 
