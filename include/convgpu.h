@@ -244,7 +244,7 @@ typedef struct cvg_multi cvg_multi;
 
 /* One context per listed CUDA device (a device may be listed more than once:
  * independent contexts sharing one GPU).  Partition weights default to the
- * measured per-unit costs of one B200 (0.92 ns per triggered column, 0.165
+ * measured per-unit costs of one B200 (0.99 ns per triggered column, 0.148
  * ns per column; tools/fit_partition.py). */
 cvg_status cvg_multi_create(const int* devices, int n_devices, cvg_multi** out);
 void cvg_multi_free(cvg_multi* m);

@@ -1507,8 +1507,8 @@ cvg_status cvg_plan_partition(long long n, const double* s, double thr, int n_pa
 
 struct cvg_multi {
   std::vector<cvg_context*> ctx;
-  double deep_weight = 0.92;     // measured ns per triggered column (multigpu.py, tools/fit_partition.py)
-  double shallow_weight = 0.165; // measured ns per column
+  double deep_weight = 0.99;     // measured ns per triggered column (multigpu.py, tools/fit_partition.py)
+  double shallow_weight = 0.148; // measured ns per column
 };
 
 namespace {

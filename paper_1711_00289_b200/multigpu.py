@@ -24,11 +24,11 @@ BYTES_PER_COLUMN_30 = 1482.0
 # Measured per-unit step times on one B200 at L = 30 (the analogue of the
 # reference's calibrate(), hetero.cpp:110-163), refit whenever the kernels
 # change (tools/fit_partition.py: c4, c5_50 and c5_05 ranges of 1/2/4/8-way
-# balanced and naive splits, each a whole step, least squares): t = 30 us +
-# 0.92 ns per triggered column + 0.165 ns per column -- a triggered column
-# weighs ~5.6 plain columns (profiles/r03_fit_partition.json).
-MEASURED_NS_PER_TRIGGERED = 0.92
-MEASURED_NS_PER_COLUMN = 0.165
+# balanced and naive splits, each a whole step, least squares): t = 31 us +
+# 0.99 ns per triggered column + 0.148 ns per column -- a triggered column
+# weighs ~6.7 plain columns (profiles/r03_fit_partition.json).
+MEASURED_NS_PER_TRIGGERED = 0.99
+MEASURED_NS_PER_COLUMN = 0.148
 
 
 def partition_weights(L: int = 30, hbm_gbs: float = 6558.7, fp64_tflops: float = 34.0, mode: str = "balanced"):
