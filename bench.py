@@ -577,8 +577,9 @@ def run_gpu_arm(args):
                        "schedule": "trigger/group compaction -> deep (main stream) || shallow + zero-fill of "
                                    "untriggered groups (side stream, concurrent)"},
         # per step: reset of the per-call words, trigger/compaction, deep, the
-        # guard-band re-derivation (relaxed path), shallow + zero-fill
-        "gpu_launches": (5 if args.variant != 2 else 4) * K,
+        # guard-band re-derivation kernel (relaxed path, calls of >= 100k
+        # columns; smaller calls re-derive inside the deep kernel), shallow
+        "gpu_launches": (5 if args.variant != 2 and n >= 100000 else 4) * K,
         "e2e": e2e,
         "feedback_loop": loop,
         "cpu_baseline": cpu,
