@@ -1,6 +1,7 @@
-// bulkcopy.cuh -- small PTX helpers of the deep kernels: shared-memory
-// addresses, the warp-per-column kernel's cp.async group-entry prefetch, and
-// the 256-bit global store of a 4-column group row.
+// bulkcopy.cuh -- small PTX helpers: shared-memory addresses, the
+// warp-per-column kernel's cp.async group-entry prefetch, the 256-bit global
+// store of a 4-column group row, and the 16-byte cp.async of the tiled shallow
+// kernel.
 #pragma once
 #include <cstdint>
 
@@ -26,6 +27,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // 256-bit global store (sm_100: STG.E.ENL2.256); p 32-byte aligned.
 __device__ __forceinline__ void st_global_v4f64(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+// 16-byte cp.async global -> shared, L1 bypassed (both 16-byte aligned).
+__device__ __forceinline__ void cp_async16_u32(unsigned dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src_gmem) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 }  // namespace cvg

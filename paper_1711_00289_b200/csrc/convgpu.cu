@@ -199,6 +199,11 @@ struct cvg_context {
   bool overlap = true;     // CVG_OVERLAP: deep || shallow on two streams
   int deep_warps = 0;      // CVG_DEEP_WARPS: 12, 16 or 20 warps per deep block (0: by mode)
   int shallow_minb = 8;    // CVG_SHALLOW_MINB: shallow blocks per SM the register budget targets (8, 12, 16)
+  // CVG_SHALLOW_TILE: the overlapped step's shallow kernel as one persistent
+  // block per SM of warp-private TMA-staged tiles (shallow_tile_kernel), with
+  // the register file it frees given to the deep block (CVG_TILE_NW warps, build-time)
+  int shallow_tile = 1;
+  int tile_warps = 8;      // CVG_TILE_WARPS: warps (= tiles in flight) of a shallow tile block
   bool strict = false;     // CVG_STRICT: reference rounding in every Newton update (all variants)
   // CVG_CARVEOUT: shared-memory carveout (% of the 228 KB maximum) preferred
   // by the deep and the shallow kernel.  One value for both: an SM runs the
@@ -251,6 +256,10 @@ struct cvg_context {
   std::vector<void*> retired;  // grown-out workspace buffers (graphs may reference them)
   std::string last_deep_kernel;  // the deep kernel the last call launched (cvg_last_deep_kernel)
 };
+
+#ifndef CVG_TILE_NW
+#define CVG_TILE_NW 24
+#endif
 
 namespace {
 
@@ -326,6 +335,11 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // overlap layout only when a shallow (or zero-fill) kernel shares the SMs
   const bool ov = ctx->overlap && dp && (sh || !fused);
   const cudaStream_t main = st;
+  // the tiled shallow kernel: overlapped deep + shallow calls whose tile
+  // stages fit beside the deep block's tables (L <= 36 at 8 warps)
+  const int tile_warps = ctx->tile_warps;
+  const size_t tile_smem = cvg::shallow_tile_table_bytes() + (size_t)tile_warps * cvg::shallow_tile_stage_bytes(b.L);
+  const bool tile = ov && sh && !fused && ctx->shallow_tile != 0 && !b.trace && tile_smem <= 150 * 1024;
   if (ov) CVG_CUDA(cudaEventRecord(w.ev_fork, st));
   // Thread-per-column deep kernel for large calls (the f02 grid on one or
   // two GPUs): 0.445 vs 0.508 ms per f02 step, 0.234 vs 0.251 ms on a 2-way
@@ -380,6 +394,13 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     } else if (tpc) {
       nwt = ov ? 12 : 10;
       kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
+    } else if (ov && tile) {
+      constexpr int NWT = CVG_TILE_NW;   // deep warps beside the tiled shallow block
+      nwt = NWT;
+      if (a.tree_precip)
+        kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, NWT, 64, 2, false>
+               : lpc_n == 8 ? cvg::deep_tpc_kernel<VAR, NWT, 64, 8, false> : cvg::deep_tpc_kernel<VAR, NWT, 64, 4, false>;
+      else kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, NWT, 64, 2> : cvg::deep_tpc_kernel<VAR, NWT, 64, 4>;
     } else if (ov) {
       nwt = 16;
       if (a.tree_precip)
@@ -399,7 +420,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
                             ",k_order_precip=" + (tpc || !a.tree_precip ? "1" : "0") + ",warps=" +
                             std::to_string(nwt) + ",blocks_per_sm=" + std::to_string(blocks) + ">";
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
+    CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, tile ? 100 : ctx->carveout));
     kern<<<ctx->num_sms * blocks, nwt * 32, smem, st>>>(a);
     CVG_CUDA(cudaGetLastError());
   } else if (dp) {
@@ -449,7 +470,12 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     } else if (dp && !fused) {   // (the feedback loop leaves untriggered columns untouched)
       k = cvg::shallow_kernel<VAR, false, true>;
     }
-    if (k) {
+    if (tile) {
+      void (*tk)(cvg::ShallowArgs) = relax ? cvg::shallow_tile_kernel<VAR, true, true> : cvg::shallow_tile_kernel<VAR, true, false>;
+      CVG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
+      CVG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      tk<<<ctx->num_sms, tile_warps * 32, tile_smem, st>>>(b);
+    } else if (k) {
       // same carveout as the deep kernel (launch_deep_t)
       CVG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
       k<<<blocks, cvg::kShallowThreads, 0, st>>>(b);
@@ -553,6 +579,8 @@ void enqueue(cvg_context* ctx, Workspace& w, const cvg_columns* in, const cvg_op
     b.d_tend_T = deep->tend_T; b.d_tend_q = deep->tend_q; b.d_precip = deep->precip;
     b.d_work = deep->work_units; b.d_exited = deep->exited_early; b.d_ld_out = deep->ld;
   }
+  b.tile_cursor = w.cursor.p + 8;
+  b.bulk_ok = ((uintptr_t)in->T & 15) == 0 && ((uintptr_t)in->q & 15) == 0 && in->ld % 2 == 0;
   b.err = w.err.p + 1; b.gl_tab = ctx->gl_tab; b.exp_tab1 = ctx->exp_tab1.p; b.first_col = in->first_col;
   b.thr = o->activity_threshold; b.L = L;
   if (fu) {
@@ -723,6 +751,8 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_REDO_INLINE")) ctx->redo_inline = atoi(e);
     if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
+    if (const char* e = getenv("CVG_SHALLOW_TILE")) ctx->shallow_tile = atoi(e);
+    if (const char* e = getenv("CVG_TILE_WARPS")) ctx->tile_warps = std::max(1, std::min(cvg::kTileWarpsMax, atoi(e)));
     if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
     if (const char* e = getenv("CVG_SLOTS")) ctx->slots = std::max(1, std::min(kSlots, atoi(e)));
     ctx->trace_path = getenv("CVG_TRACE");
@@ -1312,6 +1342,7 @@ cvg_status cvg_timestep(cvg_context* ctx, long long n, int L, long long ld, cons
     const Fused fu{leg.T.p, leg.q.p, words.p};
     std::vector<unsigned long long> h_err(2 * K);
     std::vector<unsigned> h_bad(K);
+    CVG_CUDA(cudaEventRecord(ctx->ev0, st));   // stats->device_ms: the stepping region (no state transfers)
     for (int t0 = 0; t0 < n_steps && n > 0; t0 += K) {
       const int kk = std::min(K, n_steps - t0);
       for (int j = 0; j < kk; ++j) {
@@ -1333,12 +1364,18 @@ cvg_status cvg_timestep(cvg_context* ctx, long long n, int L, long long ld, cons
         if (h_bad[j]) return fail(CVG_ERR_CHECK, "timestep: state diverged at step " + std::to_string(t0 + j));
       }
     }
+    CVG_CUDA(cudaEventRecord(ctx->ev1, st));
     if (n > 0) {
       CVG_CUDA(cudaMemcpy2DAsync(T, sizeof(double) * ld, leg.T.p, sizeof(double) * n, sizeof(double) * n, L, kout, st));
       CVG_CUDA(cudaMemcpy2DAsync(q, sizeof(double) * ld, leg.q.p, sizeof(double) * n, sizeof(double) * n, L, kout, st));
     }
     CVG_CUDA(cudaStreamSynchronize(st));
-    if (stats) stats->n_columns = n;
+    if (stats) {
+      stats->n_columns = n;
+      float ms = 0.f;
+      CVG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+      stats->device_ms = ms;
+    }
     return CVG_OK;
   });
 }

@@ -36,10 +36,14 @@ def main():
     ap.add_argument("--opts", default="")
     ap.add_argument("--slice", default=None, help="R/W: rank R's share of a W-way partition")
     ap.add_argument("--kernels", action="store_true", help="also a profiled pass (per-kernel medians)")
+    ap.add_argument("--thr", type=float, default=None,
+                    help="activity threshold override (2.0: nothing triggers -- the shallow kernel alone)")
     ap.add_argument("specs", nargs="+")
     a = ap.parse_args()
     thr = G.config_threshold(a.config)
     s, T, q = G.make_config(a.config, seed=42)
+    if a.thr is not None:
+        thr = a.thr
     L = T.shape[0]
     if a.slice:
         from paper_1711_00289_b200 import multigpu
