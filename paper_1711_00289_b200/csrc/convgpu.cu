@@ -258,7 +258,10 @@ struct cvg_context {
 };
 
 #ifndef CVG_TILE_NW
-#define CVG_TILE_NW 24
+#define CVG_TILE_NW 21
+#endif
+#ifndef CVG_TILE_REGS
+#define CVG_TILE_REGS 64
 #endif
 
 namespace {
@@ -339,7 +342,16 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // stages fit beside the deep block's tables (L <= 36 at 8 warps)
   const int tile_warps = ctx->tile_warps;
   const size_t tile_smem = cvg::shallow_tile_table_bytes() + (size_t)tile_warps * cvg::shallow_tile_stage_bytes(b.L);
-  const bool tile = ov && sh && !fused && ctx->shallow_tile != 0 && !b.trace && tile_smem <= 150 * 1024;
+  // (below ~64k columns a warp gets only a tile or two and the thread-per-
+  // column kernel's finer grain wins: c2 0.030 vs 0.033 ms; CVG_SHALLOW_TILE=2 forces it)
+  const bool tile = ov && sh && !fused && !b.trace && tile_smem <= 150 * 1024 &&
+                    (ctx->shallow_tile == 2 || (ctx->shallow_tile == 1 && b.n >= 65536));
+  // The fork stays AFTER the trigger kernel although the shallow kernel only
+  // needs the per-call words reset: launched ahead of the deep block, the
+  // shallow warps are the older ones on every SM and win the issue slots
+  // (measured: shallow done 0.1 ms early, f02 step 0.393 -> 0.411 ms; the
+  // thread-per-column shallow kernel even fills the SMs before the deep
+  // blocks arrive, 0.65 ms).
   if (ov) CVG_CUDA(cudaEventRecord(w.ev_fork, st));
   // Thread-per-column deep kernel for large calls (the f02 grid on one or
   // two GPUs): 0.445 vs 0.508 ms per f02 step, 0.234 vs 0.251 ms on a 2-way
@@ -395,12 +407,12 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
       nwt = ov ? 12 : 10;
       kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
     } else if (ov && tile) {
-      constexpr int NWT = CVG_TILE_NW;   // deep warps beside the tiled shallow block
+      constexpr int NWT = CVG_TILE_NW, RC = CVG_TILE_REGS;   // deep warps x registers beside the tiled shallow block
       nwt = NWT;
       if (a.tree_precip)
-        kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, NWT, 64, 2, false>
-               : lpc_n == 8 ? cvg::deep_tpc_kernel<VAR, NWT, 64, 8, false> : cvg::deep_tpc_kernel<VAR, NWT, 64, 4, false>;
-      else kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, NWT, 64, 2> : cvg::deep_tpc_kernel<VAR, NWT, 64, 4>;
+        kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, NWT, RC, 2, false>
+               : lpc_n == 8 ? cvg::deep_tpc_kernel<VAR, NWT, RC, 8, false> : cvg::deep_tpc_kernel<VAR, NWT, RC, 4, false>;
+      else kern = lpc_n == 2 ? cvg::deep_tpc_kernel<VAR, NWT, RC, 2> : cvg::deep_tpc_kernel<VAR, NWT, RC, 4>;
     } else if (ov) {
       nwt = 16;
       if (a.tree_precip)

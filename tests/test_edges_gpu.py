@@ -446,8 +446,8 @@ def test_capture_refuses_workspace_growth():
 
 
 @pytest.mark.parametrize("env", [{}, {"CVG_DEEP_LPC": "2"}, {"CVG_DEEP_TPC": "1"}, {"CVG_DEEP_LPC": "0", "CVG_DEEP_TPC": "0"},
-                                 {"CVG_REDO_INLINE": "0"}, {"CVG_OVERLAP": "0"}],
-                         ids=["default", "lpc2", "tpc", "warp", "redo_kernel", "serial"])
+                                 {"CVG_REDO_INLINE": "0"}, {"CVG_OVERLAP": "0"}, {"CVG_SHALLOW_TILE": "2"}],
+                         ids=["default", "lpc2", "tpc", "warp", "redo_kernel", "serial", "tile_plain_loads"])
 @pytest.mark.parametrize("variant,strict", [(0, False), (1, False), (2, False), (0, True)])
 def test_writes_stay_in_bounds_and_cover_outputs(env, variant, strict):
     """Canary check (compute-sanitizer is unavailable on this pool): every
@@ -508,3 +508,43 @@ def test_writes_stay_in_bounds_and_cover_outputs(env, variant, strict):
     od = O.convection("deep", s, T, q, O.Options(variant=variant))
     assert np.array_equal(outs[0][3].cpu().numpy(), od.work)
     c.close()
+
+
+@pytest.mark.parametrize("n,pad", [(1037, 3), (4096 + 5, 27), (2048, 0), (31, 1)])
+@pytest.mark.parametrize("variant,strict", [(0, False), (1, False), (2, False), (0, True)])
+def test_tiled_shallow_kernel_matches_thread_per_column(n, pad, variant, strict):
+    """shallow_tile_kernel forced at small sizes (default from 64k columns):
+    cp.async-staged tiles on aligned rows (even pitch), plain loads on an odd
+    pitch, ragged last tiles; outputs bit-identical to the thread-per-column
+    kernel's (same column code) and within the parity rule of the oracle."""
+    import torch
+    from conftest import env_context
+    dev = torch.device("cuda", 0)
+    L = 30
+    s, T, q = G.make_config("c1", n=n, seed=45)
+    ld = n + pad
+    o = P.KernelOptions(variant=variant, strict=strict)
+    got = []
+    for env in ({"CVG_SHALLOW_TILE": "2"}, {"CVG_SHALLOW_TILE": "0"}):
+        c = env_context(**env)
+        ds = torch.from_numpy(s).to(dev)
+        Tb = torch.zeros((L, ld), dtype=torch.float64, device=dev)
+        qb = torch.zeros((L, ld), dtype=torch.float64, device=dev)
+        Tb[:, :n] = torch.from_numpy(T)
+        qb[:, :n] = torch.from_numpy(q)
+        outs = [(torch.zeros((L, ld), dtype=torch.float64, device=dev)[:, :n],
+                 torch.zeros((L, ld), dtype=torch.float64, device=dev)[:, :n],
+                 torch.zeros(n, dtype=torch.float64, device=dev), torch.zeros(n, dtype=torch.int64, device=dev),
+                 torch.zeros(n, dtype=torch.uint8, device=dev)) for _ in range(2)]
+        c.convect_async(ds, Tb[:, :n], qb[:, :n], outs[0], outs[1], o)
+        c.check()
+        got.append([P.ColumnOutputs(*[t.cpu().numpy() for t in oo]) for oo in outs])
+        c.close()
+    for a, b in zip(got[0], got[1]):
+        for f in ("tend_T", "tend_q", "precip", "work_units", "exited_early"):
+            x, y = getattr(a, f), getattr(b, f)
+            assert np.array_equal(x.view(np.int64) if x.dtype == np.float64 else x,
+                                  y.view(np.int64) if y.dtype == np.float64 else y), f
+    oo = O.Options(variant=variant)
+    both_close(got[0][0], O.convection("deep", s, T, q, oo))
+    both_close(got[0][1], O.convection("shallow", s, T, q, oo))
