@@ -382,6 +382,7 @@ def run_gpu_arm(args):
     ms_local = ev0.elapsed_time(ev1)
     step_stats = ctx.check(stream)
     deep_kernel = ctx.last_deep_kernel
+    shallow_kernel = ctx.last_shallow_kernel
 
     def timed_pass(o, k=K):   # ms per step of k steps with options o (untimed by the contract)
         for _ in range(2):
@@ -573,8 +574,9 @@ def run_gpu_arm(args):
                           "frac_fp64_model": 1e3 * t_flop / (ms_total / K), "frac_hbm": 1e3 * t_hbm / (ms_total / K),
                           "note": "job FLOPs and bytes over all ranks / N GPUs; frac = roofline time / max-over-ranks step time"},
         "kernels_ms": {"trigger_groups": trig_ms, "deep": deep_ms, "shallow_tail_after_deep": sh_ms,
-                       "schedule": "trigger/group compaction -> deep (main stream) || shallow + zero-fill of "
-                                   "untriggered groups (side stream, concurrent)"},
+                       "deep_kernel": deep_kernel, "shallow_kernel": shallow_kernel,
+                       "schedule": "trigger/group compaction -> deep (main stream, programmatic dependent launch) || "
+                                   "shallow + zero-fill of untriggered groups (side stream, concurrent)"},
         # per step: reset of the per-call words, trigger/compaction, deep, the
         # guard-band re-derivation kernel (relaxed path, calls of >= 100k
         # columns; smaller calls re-derive inside the deep kernel), shallow

@@ -135,6 +135,7 @@ const char* cvg_version(void);
 const char* cvg_last_error(void);
 /* The deep kernel (and its launch shape) of the context's last call. */
 const char* cvg_last_deep_kernel(const cvg_context* ctx);
+const char* cvg_last_shallow_kernel(const cvg_context* ctx);   /* likewise, the shallow kernel */
 void cvg_default_options(cvg_options* opts);
 
 /* Creates a context on CUDA device `device` (requires compute capability 10.x). */
@@ -244,7 +245,7 @@ typedef struct cvg_multi cvg_multi;
 
 /* One context per listed CUDA device (a device may be listed more than once:
  * independent contexts sharing one GPU).  Partition weights default to the
- * measured per-unit costs of one B200 (0.99 ns per triggered column, 0.148
+ * measured per-unit costs of one B200 (0.86 ns per triggered column, 0.154
  * ns per column; tools/fit_partition.py). */
 cvg_status cvg_multi_create(const int* devices, int n_devices, cvg_multi** out);
 void cvg_multi_free(cvg_multi* m);

@@ -146,6 +146,8 @@ def load_library():
     if hasattr(L, "cvg_last_deep_kernel"):
         L.cvg_last_deep_kernel.restype = C.c_char_p
         L.cvg_last_deep_kernel.argtypes = [vp]
+        L.cvg_last_shallow_kernel.restype = C.c_char_p
+        L.cvg_last_shallow_kernel.argtypes = [vp]
     L.cvg_default_options.argtypes = [C.POINTER(KernelOptions)]
     L.cvg_context_create.argtypes = [i32, C.POINTER(vp)]
     L.cvg_context_free.argtypes = [vp]
@@ -419,6 +421,11 @@ class Context:
     def last_deep_kernel(self) -> str:
         """The deep kernel (and launch shape) of this context's last call."""
         return load_library().cvg_last_deep_kernel(self._h).decode()
+
+    @property
+    def last_shallow_kernel(self) -> str:
+        """The shallow kernel of this context's last call."""
+        return load_library().cvg_last_shallow_kernel(self._h).decode()
 
     def fp64_peak_tflops(self, reps: int = 5) -> float:
         v = C.c_double()

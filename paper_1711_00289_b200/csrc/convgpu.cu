@@ -204,6 +204,7 @@ struct cvg_context {
   // the register file it frees given to the deep block (CVG_TILE_NW warps, build-time)
   int shallow_tile = 1;
   int tile_warps = 8;      // CVG_TILE_WARPS: warps (= tiles in flight) of a shallow tile block
+  bool pdl = true;         // CVG_PDL: the split-column deep kernel as a programmatic dependent launch behind the trigger kernel
   bool strict = false;     // CVG_STRICT: reference rounding in every Newton update (all variants)
   // CVG_CARVEOUT: shared-memory carveout (% of the 228 KB maximum) preferred
   // by the deep and the shallow kernel.  One value for both: an SM runs the
@@ -255,6 +256,7 @@ struct cvg_context {
   bool reset_kernel = true;   // CVG_RESET_KERNEL: one reset launch instead of three memsets
   std::vector<void*> retired;  // grown-out workspace buffers (graphs may reference them)
   std::string last_deep_kernel;  // the deep kernel the last call launched (cvg_last_deep_kernel)
+  std::string last_shallow_kernel;  // ... and the shallow kernel (cvg_last_shallow_kernel)
 };
 
 #ifndef CVG_TILE_NW
@@ -342,10 +344,16 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // stages fit beside the deep block's tables (L <= 36 at 8 warps)
   const int tile_warps = ctx->tile_warps;
   const size_t tile_smem = cvg::shallow_tile_table_bytes() + (size_t)tile_warps * cvg::shallow_tile_stage_bytes(b.L);
-  // (below ~64k columns a warp gets only a tile or two and the thread-per-
-  // column kernel's finer grain wins: c2 0.030 vs 0.033 ms; CVG_SHALLOW_TILE=2 forces it)
+  // (below 32k columns a warp gets at most a tile and the thread-per-column
+  // kernel's finer grain wins: c1 0.028 vs 0.032 ms, c2 equal, c3 at 55k
+  // columns 0.0456 vs 0.0469; CVG_SHALLOW_TILE=2 forces it)
   const bool tile = ov && sh && !fused && !b.trace && tile_smem <= 150 * 1024 &&
-                    (ctx->shallow_tile == 2 || (ctx->shallow_tile == 1 && b.n >= 65536));
+                    (ctx->shallow_tile == 2 || (ctx->shallow_tile == 1 && b.n >= 32768));
+  // Programmatic dependent launch of the deep kernel: beside the tiled
+  // shallow block, alone, or on small calls.  Beside the thread-per-column
+  // shallow kernel it is a loss from ~50k columns (c3: 0.047 -> 0.052 ms; a
+  // 64k-column all-triggered share 0.101 -> 0.132 ms).
+  const bool pdl = ctx->pdl && (tile || !ov || b.n < 32768);
   // The fork stays AFTER the trigger kernel although the shallow kernel only
   // needs the per-call words reset: launched ahead of the deep block, the
   // shallow warps are the older ones on every SM and win the issue slots
@@ -433,7 +441,23 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
                             std::to_string(nwt) + ",blocks_per_sm=" + std::to_string(blocks) + ">";
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, tile ? 100 : ctx->carveout));
-    kern<<<ctx->num_sms * blocks, nwt * 32, smem, st>>>(a);
+    if (pdl) {
+      // programmatic dependent launch behind the trigger kernel: the block's
+      // table staging overlaps the trigger kernel and the launch latency
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)(ctx->num_sms * blocks));
+      cfg.blockDim = dim3((unsigned)(nwt * 32));
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CVG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    } else {
+      kern<<<ctx->num_sms * blocks, nwt * 32, smem, st>>>(a);
+    }
     CVG_CUDA(cudaGetLastError());
   } else if (dp) {
     // deep block size: kDeepWarpsOverlap leaves each SM room for three
@@ -487,7 +511,10 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
       CVG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
       CVG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       tk<<<ctx->num_sms, tile_warps * 32, tile_smem, st>>>(b);
+      ctx->last_shallow_kernel = std::string("shallow_tile_kernel<warps=") + std::to_string(tile_warps) +
+                                 ",blocks_per_sm=1,tile=32 columns,stage=cp.async>";
     } else if (k) {
+      ctx->last_shallow_kernel = sh ? "shallow_kernel<thread_per_column>" : "shallow_kernel<deep zero-fill only>";
       // same carveout as the deep kernel (launch_deep_t)
       CVG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
       k<<<blocks, cvg::kShallowThreads, 0, st>>>(b);
@@ -720,6 +747,8 @@ const char* cvg_last_error(void) { return g_last_error.c_str(); }
 
 const char* cvg_last_deep_kernel(const cvg_context* ctx) { return ctx ? ctx->last_deep_kernel.c_str() : ""; }
 
+const char* cvg_last_shallow_kernel(const cvg_context* ctx) { return ctx ? ctx->last_shallow_kernel.c_str() : ""; }
+
 void cvg_default_options(cvg_options* o) {
   if (!o) return;
   o->variant = CVG_EXACT;
@@ -764,6 +793,7 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_SHALLOW_MINB")) ctx->shallow_minb = atoi(e);
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
     if (const char* e = getenv("CVG_SHALLOW_TILE")) ctx->shallow_tile = atoi(e);
+    if (const char* e = getenv("CVG_PDL")) ctx->pdl = atoi(e) != 0;
     if (const char* e = getenv("CVG_TILE_WARPS")) ctx->tile_warps = std::max(1, std::min(cvg::kTileWarpsMax, atoi(e)));
     if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
     if (const char* e = getenv("CVG_SLOTS")) ctx->slots = std::max(1, std::min(kSlots, atoi(e)));
@@ -1556,8 +1586,8 @@ cvg_status cvg_plan_partition(long long n, const double* s, double thr, int n_pa
 
 struct cvg_multi {
   std::vector<cvg_context*> ctx;
-  double deep_weight = 0.99;     // measured ns per triggered column (multigpu.py, tools/fit_partition.py)
-  double shallow_weight = 0.148; // measured ns per column
+  double deep_weight = 0.86;     // measured ns per triggered column (multigpu.py, tools/fit_partition.py)
+  double shallow_weight = 0.154; // measured ns per column
 };
 
 namespace {

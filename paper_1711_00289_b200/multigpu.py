@@ -10,6 +10,8 @@ device timings.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import plan_partition
@@ -25,10 +27,10 @@ BYTES_PER_COLUMN_30 = 1482.0
 # reference's calibrate(), hetero.cpp:110-163), refit whenever the kernels
 # change (tools/fit_partition.py: c4, c5_50 and c5_05 ranges of 1/2/4/8-way
 # balanced and naive splits, each a whole step, least squares): t = 31 us +
-# 0.99 ns per triggered column + 0.148 ns per column -- a triggered column
-# weighs ~6.7 plain columns (profiles/r03_fit_partition.json).
-MEASURED_NS_PER_TRIGGERED = 0.99
-MEASURED_NS_PER_COLUMN = 0.148
+# 0.86 ns per triggered column + 0.154 ns per column -- a triggered column
+# weighs ~5.6 plain columns (profiles/r04_fit_partition.json, tiled shallow kernel).
+MEASURED_NS_PER_TRIGGERED = float(os.environ.get("CVG_W_TRIGGERED", 0.86))   # (overrides: calibration runs)
+MEASURED_NS_PER_COLUMN = float(os.environ.get("CVG_W_COLUMN", 0.154))
 
 
 def partition_weights(L: int = 30, hbm_gbs: float = 6558.7, fp64_tflops: float = 34.0, mode: str = "balanced"):

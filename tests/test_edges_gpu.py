@@ -446,8 +446,9 @@ def test_capture_refuses_workspace_growth():
 
 
 @pytest.mark.parametrize("env", [{}, {"CVG_DEEP_LPC": "2"}, {"CVG_DEEP_TPC": "1"}, {"CVG_DEEP_LPC": "0", "CVG_DEEP_TPC": "0"},
-                                 {"CVG_REDO_INLINE": "0"}, {"CVG_OVERLAP": "0"}, {"CVG_SHALLOW_TILE": "2"}],
-                         ids=["default", "lpc2", "tpc", "warp", "redo_kernel", "serial", "tile_plain_loads"])
+                                 {"CVG_REDO_INLINE": "0"}, {"CVG_OVERLAP": "0"}, {"CVG_SHALLOW_TILE": "2"},
+                                 {"CVG_PDL": "0"}],
+                         ids=["default", "lpc2", "tpc", "warp", "redo_kernel", "serial", "tile_plain_loads", "no_pdl"])
 @pytest.mark.parametrize("variant,strict", [(0, False), (1, False), (2, False), (0, True)])
 def test_writes_stay_in_bounds_and_cover_outputs(env, variant, strict):
     """Canary check (compute-sanitizer is unavailable on this pool): every
@@ -548,3 +549,26 @@ def test_tiled_shallow_kernel_matches_thread_per_column(n, pad, variant, strict)
     oo = O.Options(variant=variant)
     both_close(got[0][0], O.convection("deep", s, T, q, oo))
     both_close(got[0][1], O.convection("shallow", s, T, q, oo))
+
+
+@pytest.mark.parametrize("L", [1, 7, 33, 40])
+def test_tiled_shallow_kernel_level_counts(L):
+    """Tile stages scale with L (2 L rows of 256 bytes per warp); L = 40 does
+    not fit beside the deep block and falls back to the thread-per-column
+    kernel even when forced."""
+    from conftest import env_context
+    import torch
+    dev = torch.device("cuda", 0)
+    n = 3000 + 12   # even row pitch (cp.async path), ragged last tile
+    s, T, q = G.make_config("ref", n=n, L=L, seed=L + 100)
+    c = env_context(CVG_SHALLOW_TILE="2")
+    ds, dT, dq = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (s, T, q))
+    outs = [(torch.zeros((L, n), dtype=torch.float64, device=dev), torch.zeros((L, n), dtype=torch.float64, device=dev),
+             torch.zeros(n, dtype=torch.float64, device=dev), torch.zeros(n, dtype=torch.int64, device=dev),
+             torch.zeros(n, dtype=torch.uint8, device=dev)) for _ in range(2)]
+    c.convect_async(ds, dT, dq, outs[0], outs[1])
+    c.check()
+    assert ("shallow_tile_kernel" in c.last_shallow_kernel) == (L <= 36)
+    both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in outs[0]]), O.convection("deep", s, T, q))
+    both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in outs[1]]), O.convection("shallow", s, T, q))
+    c.close()

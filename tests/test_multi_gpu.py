@@ -52,7 +52,7 @@ def test_multi_partition_is_cost_balanced(ctx):
         m.convect(s, T, q, P.KernelOptions(), kernels=P.DEEP)
         b = m.last_bounds
     trig = np.concatenate([[0], np.cumsum(s > 0.5)])
-    cost = [0.99 * (trig[b[i + 1]] - trig[b[i]]) + 0.148 * (b[i + 1] - b[i]) for i in range(4)]
+    cost = [0.86 * (trig[b[i + 1]] - trig[b[i]]) + 0.154 * (b[i + 1] - b[i]) for i in range(4)]
     assert max(cost) / min(cost) < 1.1
     assert np.ptp(np.diff(b)) > 0.2 * s.size / 4   # not the naive equal split
 
