@@ -452,6 +452,7 @@ def run_gpu_arm(args):
     sh_ms = float(np.mean(np.maximum(kern[:, 2], 0.0))) if len(kern) else float("nan")
     achieved = deep_flops / (deep_ms * 1e-3) / 1e12
     traffic = None
+    step_traffic = None
     tf = os.path.join(ROOT, "profiles", "deep_traffic.json")
     if os.path.exists(tf):
         try:
@@ -460,6 +461,7 @@ def run_gpu_arm(args):
             # only for the kernel this run launched, profiled on this workload
             if d.get("config") == args.config and d.get("kernel_desc") == deep_kernel and ws == 1 and not args.slice:
                 traffic = d.get("dram_bytes_per_launch")
+                step_traffic = d.get("step_dram_bytes")
         except Exception:
             pass
     deep_bytes_alg = trig_r * (8 + 2 * 8 * L + 2 * 8 * L + 8 + 8 + 1)
@@ -572,7 +574,9 @@ def run_gpu_arm(args):
                           "bound": "fp64" if t_flop >= t_hbm else "hbm",
                           "roofline_ms": 1e3 * t_roof, "frac": 1e3 * t_roof / (ms_total / K),
                           "frac_fp64_model": 1e3 * t_flop / (ms_total / K), "frac_hbm": 1e3 * t_hbm / (ms_total / K),
-                          "note": "job FLOPs and bytes over all ranks / N GPUs; frac = roofline time / max-over-ranks step time"},
+                          "traffic": step_traffic,
+                          "note": "job FLOPs and bytes over all ranks / N GPUs; frac = roofline time / max-over-ranks step time; "
+                                  "traffic = ncu DRAM bytes of one step's kernels (profiles/deep_traffic.json, N=1 only)"},
         "kernels_ms": {"trigger_groups": trig_ms, "deep": deep_ms, "shallow_tail_after_deep": sh_ms,
                        "deep_kernel": deep_kernel, "shallow_kernel": shallow_kernel,
                        "schedule": "trigger/group compaction -> deep (main stream, programmatic dependent launch) || "

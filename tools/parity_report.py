@@ -2,7 +2,7 @@
 """GPU parity report: every BASELINE config at its stated size, every variant,
 every device path, EVERY column against the CPU oracle (test infrastructure).
 
-    python tools/parity_report.py --out profiles/parity_r02.json [--quick]
+    python tools/parity_report.py --out profiles/parity_r04.json [--quick]
 
 Per (config, variant, path) and kernel it records, for tend_T / tend_q /
 precip, the worst absolute and relative deviation and the number of values
@@ -72,7 +72,7 @@ def context(**env):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "parity_r02.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "parity_r04.json"))
     ap.add_argument("--quick", action="store_true", help="small grids only (smoke of the tool)")
     ap.add_argument("--seed", type=int, default=42)
     args = ap.parse_args()

@@ -95,8 +95,24 @@ if deep:
         grid = int(float(d.get("launch__grid_size", "148").split()[0]))
         desc = (f"deep_tpc_kernel<lanes_per_column={m.group(4)},k_order_precip={m.group(5)},warps={m.group(2)},"
                 f"blocks_per_sm={max(1, grid // 148)}>")
+    # DRAM bytes of one default step: the first capture of each kernel of the
+    # default schedule (trigger, deep, re-derivation, shallow)
+    def dram(x):
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            f = x[k].split()
+            tot += float(f[0]) * scale.get(f[1] if len(f) > 1 else "byte", 1)
+        return tot
+    step, seen = {}, set()
+    for x in caps:
+        base = x["kernel"].split("<")[0]
+        if base in seen:
+            continue
+        seen.add(base)
+        step[x["kernel"]] = dram(x)
     json.dump({"config": config, "tag": tag, "kernel": d["kernel"], "kernel_desc": desc,
                "dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
-               "source": f"profiles/{tag}_ncu_summary.md (ncu --set full, one launch)"},
+               "step_dram_bytes": sum(step.values()), "step_dram_bytes_by_kernel": step,
+               "source": f"profiles/{tag}_ncu_summary.md (ncu --set full, one launch of each kernel, serialised)"},
               open(os.path.join(prof, "deep_traffic.json"), "w"), indent=1)
 print("\n".join(lines))
