@@ -9,7 +9,8 @@ compute-sanitizer (one tool per run):
 c1 at 4,096 columns: trigger + compaction, every deep kernel
 (split 2/4/8 lanes, thread- and warp-per-column), every variant, the strict
 and no-far32 paths, the guard-band re-derivation (redo_kernel, and inline),
-the shallow kernel with and without the deep zero-fill, the host-buffer
+the shallow kernel with and without the deep zero-fill, the tiled shallow
+kernel (forced at this size), programmatic and plain deep launches, the host-buffer
 pipeline with small chunks, the fused feedback loop (deep and shallow),
 error growth, the multi-device engine, the batched ientropy / exp entry
 points and a latched failure.  Results are checked against the oracle at the
@@ -38,7 +39,8 @@ def main():
     checks = 0
     envs = [{}, {"CVG_DEEP_LPC": "2"}, {"CVG_DEEP_LPC": "4"}, {"CVG_DEEP_LPC": "8"}, {"CVG_DEEP_TPC": "1"},
             {"CVG_DEEP_LPC": "0", "CVG_DEEP_TPC": "0"}, {"CVG_REDO_INLINE": "1"}, {"CVG_OVERLAP": "0"},
-            {"CVG_CHUNK_COLS": "1000"}]
+            {"CVG_CHUNK_COLS": "1000"}, {"CVG_SHALLOW_TILE": "2"}, {"CVG_SHALLOW_TILE": "2", "CVG_TILE_WARPS": "3"},
+            {"CVG_PDL": "0"}]
     for env in envs:
         ctx = env_context(**env)
         for variant in (0, 1, 2):
