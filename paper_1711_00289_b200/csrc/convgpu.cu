@@ -204,6 +204,8 @@ struct cvg_context {
   // the register file it frees given to the deep block (CVG_TILE_NW warps, build-time)
   int shallow_tile = 1;
   int tile_warps = 8;      // CVG_TILE_WARPS: warps (= tiles in flight) of a shallow tile block
+  int tile_warps_alone = 12;  // CVG_TILE_WARPS_ALONE: ... of a shallow-only call (no deep block beside it)
+  int deep_only = -1;      // CVG_DEEP_ONLY: schedule of deep-only calls (launch_kernels; -1 by size)
   bool pdl = true;         // CVG_PDL: the split-column deep kernel as a programmatic dependent launch behind the trigger kernel
   bool strict = false;     // CVG_STRICT: reference rounding in every Newton update (all variants)
   // CVG_CARVEOUT: shared-memory carveout (% of the 228 KB maximum) preferred
@@ -338,7 +340,15 @@ template <int VAR>
 void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, const cvg::ShallowArgs& b, bool sh,
                     bool dp, cudaEvent_t* pe, cudaStream_t st, bool strict, bool fused) {
   // overlap layout only when a shallow (or zero-fill) kernel shares the SMs
-  const bool ov = ctx->overlap && dp && (sh || !fused);
+  // deep-only calls (sh false, the zero-fill kernel beside the deep one):
+  // CVG_DEEP_ONLY 0 = overlapped beside a 16-warp deep block, 1 = serial (two
+  // 16-warp deep blocks per SM, then the zero-fill), 2 = overlapped beside the
+  // 21-warp deep block of the tiled schedule
+  // (-1, default: by size -- f02 0.384 / 0.354 / 0.355 ms, c5_95 0.95 / 0.79 /
+  // 0.85, an 88k-column share 0.0725 / 0.0726 / 0.0668, c2 0.029 / 0.053 / 0.030)
+  const int deep_only = ctx->deep_only >= 0 ? ctx->deep_only : (a.n >= 400000 ? 1 : a.n >= 32768 ? 2 : 0);
+  const bool ov = ctx->overlap && dp && (sh || (!fused && deep_only != 1));
+  const bool wide_deep_only = ov && !sh && !fused && deep_only == 2;
   const cudaStream_t main = st;
   // the tiled shallow kernel: overlapped deep + shallow calls whose tile
   // stages fit beside the deep block's tables (L <= 36 at 8 warps)
@@ -414,7 +424,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     } else if (tpc) {
       nwt = ov ? 12 : 10;
       kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
-    } else if (ov && tile) {
+    } else if (ov && (tile || wide_deep_only)) {
       constexpr int NWT = CVG_TILE_NW, RC = CVG_TILE_REGS;   // deep warps x registers beside the tiled shallow block
       nwt = NWT;
       if (a.tree_precip)
@@ -506,12 +516,27 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     } else if (dp && !fused) {   // (the feedback loop leaves untriggered columns untouched)
       k = cvg::shallow_kernel<VAR, false, true>;
     }
-    if (tile) {
-      void (*tk)(cvg::ShallowArgs) = relax ? cvg::shallow_tile_kernel<VAR, true, true> : cvg::shallow_tile_kernel<VAR, true, false>;
-      CVG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
+    // shallow-only calls: the tiled kernel alone on the SM, with as many
+    // warps (tiles in flight) as its stages fit (CVG_TILE_WARPS_ALONE)
+    int alone_warps = ctx->tile_warps_alone;
+    while (alone_warps > 1 && cvg::shallow_tile_table_bytes() + (size_t)alone_warps * cvg::shallow_tile_stage_bytes(b.L) >
+                                  200 * 1024)
+      --alone_warps;
+    // (f02: 0.148 ms against the thread-per-column kernel's 0.236 -- 871 MB at
+    // 5.9 TB/s, 90 % of the measured HBM copy bandwidth; 188k columns 0.040 vs
+    // 0.064, 123k 0.031 vs 0.033, 88k 0.025 vs 0.023: from 100k columns)
+    const bool tile_alone = sh && !dp && !fused && !b.trace && alone_warps >= 4 &&
+                            (ctx->shallow_tile == 2 || (ctx->shallow_tile == 1 && b.n >= 100000));
+    if (tile || tile_alone) {
+      void (*tk)(cvg::ShallowArgs) =
+          tile ? (relax ? cvg::shallow_tile_kernel<VAR, true, true> : cvg::shallow_tile_kernel<VAR, true, false>)
+               : (relax ? cvg::shallow_tile_kernel<VAR, false, true> : cvg::shallow_tile_kernel<VAR, false, false>);
+      const int tw = tile ? tile_warps : alone_warps;
+      const size_t smem = cvg::shallow_tile_table_bytes() + (size_t)tw * cvg::shallow_tile_stage_bytes(b.L);
+      CVG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       CVG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      tk<<<ctx->num_sms, tile_warps * 32, tile_smem, st>>>(b);
-      ctx->last_shallow_kernel = std::string("shallow_tile_kernel<warps=") + std::to_string(tile_warps) +
+      tk<<<ctx->num_sms, tw * 32, smem, st>>>(b);
+      ctx->last_shallow_kernel = std::string("shallow_tile_kernel<warps=") + std::to_string(tw) +
                                  ",blocks_per_sm=1,tile=32 columns,stage=cp.async>";
     } else if (k) {
       ctx->last_shallow_kernel = sh ? "shallow_kernel<thread_per_column>" : "shallow_kernel<deep zero-fill only>";
@@ -794,6 +819,9 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
     if (const char* e = getenv("CVG_SHALLOW_TILE")) ctx->shallow_tile = atoi(e);
     if (const char* e = getenv("CVG_PDL")) ctx->pdl = atoi(e) != 0;
+    if (const char* e = getenv("CVG_TILE_WARPS_ALONE"))
+      ctx->tile_warps_alone = std::max(1, std::min(cvg::kTileWarpsMax, atoi(e)));
+    if (const char* e = getenv("CVG_DEEP_ONLY")) ctx->deep_only = atoi(e);
     if (const char* e = getenv("CVG_TILE_WARPS")) ctx->tile_warps = std::max(1, std::min(cvg::kTileWarpsMax, atoi(e)));
     if (const char* e = getenv("CVG_CHUNK_COLS")) ctx->chunk_cols = std::max(1LL, atoll(e));
     if (const char* e = getenv("CVG_SLOTS")) ctx->slots = std::max(1, std::min(kSlots, atoi(e)));

@@ -572,3 +572,34 @@ def test_tiled_shallow_kernel_level_counts(L):
     both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in outs[0]]), O.convection("deep", s, T, q))
     both_close(P.ColumnOutputs(*[t.cpu().numpy() for t in outs[1]]), O.convection("shallow", s, T, q))
     c.close()
+
+
+@pytest.mark.parametrize("variant,strict", [(0, False), (2, False), (0, True)])
+def test_tiled_shallow_kernel_alone(variant, strict):
+    """Shallow-only calls run the tiled kernel alone on the SM (12 warps per
+    block, no deep zero-fill): forced at a small ragged size, bit-identical
+    to the thread-per-column kernel; deep outputs are not touched."""
+    import torch
+    from conftest import env_context
+    dev = torch.device("cuda", 0)
+    n, L = 5000 + 6, 30
+    s, T, q = G.make_config("c1", n=n, seed=46)
+    o = P.KernelOptions(variant=variant, strict=strict)
+    got = []
+    for env in ({"CVG_SHALLOW_TILE": "2"}, {"CVG_SHALLOW_TILE": "0"}):
+        c = env_context(**env)
+        ds, dT, dq = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (s, T, q))
+        outs = [(torch.full((L, n), 7.0, dtype=torch.float64, device=dev), torch.full((L, n), 7.0, dtype=torch.float64, device=dev),
+                 torch.full((n,), 7.0, dtype=torch.float64, device=dev), torch.full((n,), 7, dtype=torch.int64, device=dev),
+                 torch.full((n,), 7, dtype=torch.uint8, device=dev)) for _ in range(2)]
+        c.convect_async(ds, dT, dq, outs[0], outs[1], o, P.SHALLOW)
+        c.check()
+        assert ("shallow_tile_kernel<warps=12" in c.last_shallow_kernel) == (env["CVG_SHALLOW_TILE"] == "2")
+        assert all(bool((t == 7).all()) for t in outs[0]), "a shallow-only call wrote a deep output"
+        got.append(P.ColumnOutputs(*[t.cpu().numpy() for t in outs[1]]))
+        c.close()
+    for f in ("tend_T", "tend_q", "precip", "work_units", "exited_early"):
+        x, y = getattr(got[0], f), getattr(got[1], f)
+        assert np.array_equal(x.view(np.int64) if x.dtype == np.float64 else x,
+                              y.view(np.int64) if y.dtype == np.float64 else y), f
+    both_close(got[0], O.convection("shallow", s, T, q, O.Options(variant=variant)))

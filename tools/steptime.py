@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--opts", default="")
     ap.add_argument("--slice", default=None, help="R/W: rank R's share of a W-way partition")
     ap.add_argument("--kernels", action="store_true", help="also a profiled pass (per-kernel medians)")
+    ap.add_argument("--mask", default="both", choices=["both", "deep", "shallow"], help="kernels of the call")
     ap.add_argument("--thr", type=float, default=None,
                     help="activity threshold override (2.0: nothing triggers -- the shallow kernel alone)")
     ap.add_argument("specs", nargs="+")
@@ -70,6 +71,7 @@ def main():
     for o in filter(None, a.opts.split(",")):
         kw.update(flags[o])
     opts = P.KernelOptions(variant=a.variant, activity_threshold=thr, **kw)
+    MASK = {"both": P.BOTH, "deep": P.DEEP, "shallow": P.SHALLOW}[a.mask]
     stream = torch.cuda.Stream(device=dev)
     runs = []
     for spec in a.specs:
@@ -77,7 +79,7 @@ def main():
         env = dict(e.split("=", 1) for e in envs.split(",") if e)
         ctx = env_context(**env)
         for _ in range(3):
-            ctx.convect_async(ds, dT, dq, outs[0], outs[1], opts, P.BOTH, stream=stream)
+            ctx.convect_async(ds, dT, dq, outs[0], outs[1], opts, MASK, stream=stream)
         st = ctx.check(stream)
         runs.append((label, ctx, [], st))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -86,7 +88,7 @@ def main():
             torch.cuda.synchronize()
             ev0.record(stream)
             for _ in range(a.steps):
-                ctx.convect_async(ds, dT, dq, outs[0], outs[1], opts, P.BOTH, stream=stream)
+                ctx.convect_async(ds, dT, dq, outs[0], outs[1], opts, MASK, stream=stream)
             ev1.record(stream)
             stream.synchronize()
             ts.append(ev0.elapsed_time(ev1) / a.steps)
@@ -96,7 +98,7 @@ def main():
         if a.kernels:   # one profiled pass: event pairs between the kernels
             ctx.profile_begin(a.steps)
             for _ in range(a.steps):
-                ctx.convect_async(ds, dT, dq, outs[0], outs[1], opts, P.BOTH, stream=stream)
+                ctx.convect_async(ds, dT, dq, outs[0], outs[1], opts, MASK, stream=stream)
             stream.synchronize()
             k = ctx.profile_end(a.steps)
             kern = "  trig %.4f deep %.4f shallow(after deep) %.4f" % tuple(np.median(k, axis=0))
