@@ -357,7 +357,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // (below 32k columns a warp gets at most a tile and the thread-per-column
   // kernel's finer grain wins: c1 0.028 vs 0.032 ms, c2 equal, c3 at 55k
   // columns 0.0456 vs 0.0469; CVG_SHALLOW_TILE=2 forces it)
-  const bool tile = ov && sh && !fused && !b.trace && tile_smem <= 150 * 1024 &&
+  const bool tile = ov && sh && !fused && !b.trace && tile_smem + cvg::deep_table_bytes() <= 222 * 1024 &&
                     (ctx->shallow_tile == 2 || (ctx->shallow_tile == 1 && b.n >= 32768));
   // Programmatic dependent launch of the deep kernel: beside the tiled
   // shallow block, alone, or on small calls.  Beside the thread-per-column
