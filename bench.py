@@ -461,7 +461,8 @@ def run_gpu_arm(args):
             # only for the kernel this run launched, profiled on this workload
             if d.get("config") == args.config and d.get("kernel_desc") == deep_kernel and ws == 1 and not args.slice:
                 traffic = d.get("dram_bytes_per_launch")
-                step_traffic = d.get("step_dram_bytes")
+                # the range capture (kernels overlapped) when there is one, else the serialised sum
+                step_traffic = d.get("step_dram_bytes_overlapped", d.get("step_dram_bytes"))
         except Exception:
             pass
     deep_bytes_alg = trig_r * (8 + 2 * 8 * L + 2 * 8 * L + 8 + 8 + 1)
@@ -576,7 +577,7 @@ def run_gpu_arm(args):
                           "frac_fp64_model": 1e3 * t_flop / (ms_total / K), "frac_hbm": 1e3 * t_hbm / (ms_total / K),
                           "traffic": step_traffic,
                           "note": "job FLOPs and bytes over all ranks / N GPUs; frac = roofline time / max-over-ranks step time; "
-                                  "traffic = ncu DRAM bytes of one step's kernels (profiles/deep_traffic.json, N=1 only)"},
+                                  "traffic = ncu DRAM bytes of one step, range capture with the kernels overlapped (profiles/deep_traffic.json, N=1 only)"},
         "kernels_ms": {"trigger_groups": trig_ms, "deep": deep_ms, "shallow_tail_after_deep": sh_ms,
                        "deep_kernel": deep_kernel, "shallow_kernel": shallow_kernel,
                        "schedule": "trigger/group compaction -> deep (main stream, programmatic dependent launch) || "

@@ -110,7 +110,13 @@ if deep:
             continue
         seen.add(base)
         step[x["kernel"]] = dram(x)
-    json.dump({"config": config, "tag": tag, "kernel": d["kernel"], "kernel_desc": desc,
+    prev = {}
+    try:   # keep the range capture of the overlapped step (tools/step_range.py), if any
+        prev = json.load(open(os.path.join(prof, "deep_traffic.json")))
+    except Exception:
+        pass
+    keep = {k: prev[k] for k in ("step_dram_bytes_overlapped", "step_range_source") if k in prev}
+    json.dump({**keep, "config": config, "tag": tag, "kernel": d["kernel"], "kernel_desc": desc,
                "dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
                "step_dram_bytes": sum(step.values()), "step_dram_bytes_by_kernel": step,
                "source": f"profiles/{tag}_ncu_summary.md (ncu --set full, one launch of each kernel, serialised)"},
