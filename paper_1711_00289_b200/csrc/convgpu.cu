@@ -264,6 +264,9 @@ struct cvg_context {
 #ifndef CVG_TILE_NW
 #define CVG_TILE_NW 21
 #endif
+#ifndef CVG_DEEPONLY_NW
+#define CVG_DEEPONLY_NW 28
+#endif
 #ifndef CVG_TILE_REGS
 #define CVG_TILE_REGS 64
 #endif
@@ -344,11 +347,20 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   // CVG_DEEP_ONLY 0 = overlapped beside a 16-warp deep block, 1 = serial (two
   // 16-warp deep blocks per SM, then the zero-fill), 2 = overlapped beside the
   // 21-warp deep block of the tiled schedule
-  // (-1, default: by size -- f02 0.384 / 0.354 / 0.355 ms, c5_95 0.95 / 0.79 /
-  // 0.85, an 88k-column share 0.0725 / 0.0726 / 0.0668, c2 0.029 / 0.053 / 0.030)
-  const int deep_only = ctx->deep_only >= 0 ? ctx->deep_only : (a.n >= 400000 ? 1 : a.n >= 32768 ? 2 : 0);
+  // 3 = a persistent four-warp zero-fill block beside a CVG_DEEPONLY_NW-warp
+  // deep block (2 lanes per column)
+  // (-1, default: by size.  modes 0 / 1 / 2 / 3 in ms: f02 0.384 / 0.354 / 0.355
+  // / 0.317, c5_05 - / 0.161 / 0.107 / 0.101, c5_95 0.95 / 0.79 / 0.85 / 0.79, a
+  // 445k-column half - / 0.216 / 0.192 / 0.188, a 257k-column quarter - / 0.1125
+  // / 0.121 / 0.113, a 188k one - / 0.1197 / 0.1196 / 0.130 (1.1 claims per warp
+  // at 28 warps), an 88k-column eighth 0.0725 / 0.0726 / 0.0668 / -, c2 0.029 /
+  // 0.053 / 0.030 / -)
+  int deep_only = ctx->deep_only >= 0 ? ctx->deep_only
+                  : a.n >= 400000 ? 3 : a.n >= cvg::kTpcMinColumns / 2 ? 1 : a.n >= 32768 ? 2 : 0;
+  if (deep_only == 3 && (ctx->deep_lpc >= 0 || ctx->deep_tpc == 1 || a.L > 32)) deep_only = 1;   // (2-lane builds only)
   const bool ov = ctx->overlap && dp && (sh || (!fused && deep_only != 1));
   const bool wide_deep_only = ov && !sh && !fused && deep_only == 2;
+  const bool zero_beside = ov && !sh && !fused && deep_only == 3;
   const cudaStream_t main = st;
   // the tiled shallow kernel: overlapped deep + shallow calls whose tile
   // stages fit beside the deep block's tables (L <= 36 at 8 warps)
@@ -390,6 +402,7 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
   int lpc_n = ctx->deep_lpc >= 0 ? ctx->deep_lpc
                                  : (a.n >= cvg::kTpcMinColumns / 2 ? 2 : a.n >= 100000 ? 4 : 8);
   if (lpc_n == 8 && (fused || !a.tree_precip || !ov)) lpc_n = 4;   // 8 lanes: overlapped relaxed builds only
+  if (zero_beside) lpc_n = 2;
   if (fused && lpc_n <= 1 && !tpc_forced) lpc_n = 2;   // the warp-per-column kernel has no feedback-loop mode
   const bool lpc = !tpc_forced && dp && lpc_n > 1;
   const bool tpc = !lpc && dp && a.L <= 32 &&
@@ -424,6 +437,10 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     } else if (tpc) {
       nwt = ov ? 12 : 10;
       kern = ov ? cvg::deep_tpc_kernel<VAR, 12, 104> : cvg::deep_tpc_kernel<VAR, 10, 96>;
+    } else if (zero_beside) {
+      constexpr int NWZ = CVG_DEEPONLY_NW;
+      nwt = NWZ;
+      kern = a.tree_precip ? cvg::deep_tpc_kernel<VAR, NWZ, 64, 2, false> : cvg::deep_tpc_kernel<VAR, NWZ, 64, 2>;
     } else if (ov && (tile || wide_deep_only)) {
       constexpr int NWT = CVG_TILE_NW, RC = CVG_TILE_REGS;   // deep warps x registers beside the tiled shallow block
       nwt = NWT;
@@ -515,6 +532,11 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
       k = cvg::shallow_kernel<VAR, true, false>;
     } else if (dp && !fused) {   // (the feedback loop leaves untriggered columns untouched)
       k = cvg::shallow_kernel<VAR, false, true>;
+    }
+    if (zero_beside) {
+      cvg::deep_zero_kernel<<<ctx->num_sms, cvg::kZeroThreads, 0, st>>>(b);
+      ctx->last_shallow_kernel = "deep_zero_kernel<persistent,4 warps>";
+      k = nullptr;
     }
     // shallow-only calls: the tiled kernel alone on the SM, with as many
     // warps (tiles in flight) as its stages fit (CVG_TILE_WARPS_ALONE)

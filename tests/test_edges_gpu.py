@@ -603,3 +603,36 @@ def test_tiled_shallow_kernel_alone(variant, strict):
         assert np.array_equal(x.view(np.int64) if x.dtype == np.float64 else x,
                               y.view(np.int64) if y.dtype == np.float64 else y), f
     both_close(got[0], O.convection("shallow", s, T, q, O.Options(variant=variant)))
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("variant,strict", [(0, False), (2, False), (0, True)])
+def test_deep_only_schedules(mode, variant, strict):
+    """Deep-only calls (cvg_deep_convection): every schedule of the zero-fill
+    -- beside a 16-warp deep block, after two 16-warp blocks, beside the
+    21-warp block, and the persistent deep_zero_kernel beside a 28-warp block
+    (default from 400k columns, forced here) -- writes every deep output,
+    nothing else, and matches the oracle."""
+    import torch
+    from conftest import env_context
+    dev = torch.device("cuda", 0)
+    n, L = 3000 + 17, 30
+    s, T, q = G.make_config("c1", n=n, seed=47)
+    c = env_context(CVG_DEEP_ONLY=mode)
+    ds, dT, dq = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (s, T, q))
+    SENT = 12345.0
+    outs = [(torch.full((L, n), SENT, dtype=torch.float64, device=dev), torch.full((L, n), SENT, dtype=torch.float64, device=dev),
+             torch.full((n,), SENT, dtype=torch.float64, device=dev), torch.full((n,), 7, dtype=torch.int64, device=dev),
+             torch.full((n,), 7, dtype=torch.uint8, device=dev)) for _ in range(2)]
+    c.convect_async(ds, dT, dq, outs[0], outs[1], P.KernelOptions(variant=variant, strict=strict), P.DEEP)
+    c.check()
+    if mode == "3":
+        assert "deep_zero_kernel" in c.last_shallow_kernel and "warps=28" in c.last_deep_kernel
+    assert not any(bool((t == SENT).any()) for t in outs[0][:3]), "a deep output element was not written"
+    assert all(bool((t == SENT).all()) for t in outs[1][:3]) and bool((outs[1][3] == 7).all()), \
+        "a deep-only call wrote a shallow output"
+    od = O.convection("deep", s, T, q, O.Options(variant=variant))
+    got = P.ColumnOutputs(*[t.cpu().numpy() for t in outs[0]])
+    both_close(got, od)
+    assert np.array_equal(got.work_units, od.work)
+    c.close()
