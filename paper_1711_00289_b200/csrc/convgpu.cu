@@ -10,6 +10,7 @@
 // taxonomy at the boundary (capi.cpp:51-89); and the multi-device partition
 // planner.  No CPU fallback exists: without a usable sm_100 device every
 // compute entry point returns CVG_ERR_DEVICE.
+#include <cuda.h>   // CUtensorMap types only: cuTensorMapEncodeTiled is fetched through the runtime (no libcuda link)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -204,6 +205,7 @@ struct cvg_context {
   // the register file it frees given to the deep block (CVG_TILE_NW warps, build-time)
   int shallow_tile = 1;
   int tile_warps = 8;      // CVG_TILE_WARPS: warps (= tiles in flight) of a shallow tile block
+  bool tile_tma = true;    // CVG_TILE_TMA: tile rows by TMA tensor tiles (0: 16-byte cp.async)
   int tile_warps_alone = 12;  // CVG_TILE_WARPS_ALONE: ... of a shallow-only call (no deep block beside it)
   int deep_only = -1;      // CVG_DEEP_ONLY: schedule of deep-only calls (launch_kernels; -1 by size)
   bool pdl = true;         // CVG_PDL: the split-column deep kernel as a programmatic dependent launch behind the trigger kernel
@@ -326,6 +328,40 @@ void launch_deep_t(cvg_context* ctx, const cvg::DeepArgs& a, cudaStream_t st) {
   CVG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, ctx->carveout));
   kern<<<ctx->num_sms, threads, smem, st>>>(a);
   CVG_CUDA(cudaGetLastError());
+}
+
+// TMA descriptors of the tiled shallow kernel: T and q as 2-D tensors
+// [L][n] of doubles (row pitch ld), box [L][32].  The driver's encoder is
+// fetched through the runtime; false when it is unavailable or the layout
+// does not qualify (the kernel then stages its tiles with cp.async).
+bool encode_tile_maps(const cvg::ShallowArgs& b, cvg::TileMaps* out) {
+  typedef CUresult (*encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static encode_fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return (encode_fn)p;
+  }();
+  static_assert(sizeof(CUtensorMap) == sizeof(out->T), "tensor map size");
+  if (!fn || !b.bulk_ok || b.L > 256 || b.n < 1) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)b.n, (cuuint64_t)b.L};
+  const cuuint64_t strides[1] = {(cuuint64_t)b.ld_in * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)cvg::kTileCols, (cuuint32_t)b.L};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int i = 0; i < 2; ++i) {
+    void* base = const_cast<double*>(i == 0 ? b.T : b.q);
+    CUtensorMap* m = reinterpret_cast<CUtensorMap*>(i == 0 ? out->T : out->q);
+    if (fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
 }
 
 // Feedback-loop mode of a call (cvg_timestep): the kernels write the
@@ -550,16 +586,19 @@ void launch_kernels(cvg_context* ctx, Workspace& w, const cvg::DeepArgs& a, cons
     const bool tile_alone = sh && !dp && !fused && !b.trace && alone_warps >= 4 &&
                             (ctx->shallow_tile == 2 || (ctx->shallow_tile == 1 && b.n >= 100000));
     if (tile || tile_alone) {
-      void (*tk)(cvg::ShallowArgs) =
+      void (*tk)(cvg::ShallowArgs, const cvg::TileMaps) =
           tile ? (relax ? cvg::shallow_tile_kernel<VAR, true, true> : cvg::shallow_tile_kernel<VAR, true, false>)
                : (relax ? cvg::shallow_tile_kernel<VAR, false, true> : cvg::shallow_tile_kernel<VAR, false, false>);
+      cvg::TileMaps maps{};
+      cvg::ShallowArgs bt = b;
+      bt.use_tma = ctx->tile_tma && encode_tile_maps(b, &maps);
       const int tw = tile ? tile_warps : alone_warps;
       const size_t smem = cvg::shallow_tile_table_bytes() + (size_t)tw * cvg::shallow_tile_stage_bytes(b.L);
       CVG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       CVG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      tk<<<ctx->num_sms, tw * 32, smem, st>>>(b);
+      tk<<<ctx->num_sms, tw * 32, smem, st>>>(bt, maps);
       ctx->last_shallow_kernel = std::string("shallow_tile_kernel<warps=") + std::to_string(tw) +
-                                 ",blocks_per_sm=1,tile=32 columns,stage=cp.async>";
+                                 ",blocks_per_sm=1,tile=32 columns,stage=" + (bt.use_tma ? "TMA" : "cp.async") + ">";
     } else if (k) {
       ctx->last_shallow_kernel = sh ? "shallow_kernel<thread_per_column>" : "shallow_kernel<deep zero-fill only>";
       // same carveout as the deep kernel (launch_deep_t)
@@ -841,6 +880,7 @@ cvg_status cvg_context_create(int device, cvg_context** out) {
     if (const char* e = getenv("CVG_DEEP_WARPS")) ctx->deep_warps = atoi(e);
     if (const char* e = getenv("CVG_SHALLOW_TILE")) ctx->shallow_tile = atoi(e);
     if (const char* e = getenv("CVG_PDL")) ctx->pdl = atoi(e) != 0;
+    if (const char* e = getenv("CVG_TILE_TMA")) ctx->tile_tma = atoi(e) != 0;
     if (const char* e = getenv("CVG_TILE_WARPS_ALONE"))
       ctx->tile_warps_alone = std::max(1, std::min(cvg::kTileWarpsMax, atoi(e)));
     if (const char* e = getenv("CVG_DEEP_ONLY")) ctx->deep_only = atoi(e);

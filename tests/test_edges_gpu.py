@@ -514,9 +514,9 @@ def test_writes_stay_in_bounds_and_cover_outputs(env, variant, strict):
 @pytest.mark.parametrize("n,pad", [(1037, 3), (4096 + 5, 27), (2048, 0), (31, 1)])
 @pytest.mark.parametrize("variant,strict", [(0, False), (1, False), (2, False), (0, True)])
 def test_tiled_shallow_kernel_matches_thread_per_column(n, pad, variant, strict):
-    """shallow_tile_kernel forced at small sizes (default from 64k columns):
-    cp.async-staged tiles on aligned rows (even pitch), plain loads on an odd
-    pitch, ragged last tiles; outputs bit-identical to the thread-per-column
+    """shallow_tile_kernel forced at small sizes (default from 32k columns):
+    TMA- and cp.async-staged tiles on aligned rows (even pitch), plain loads on
+    an odd pitch, ragged last tiles; outputs bit-identical to the thread-per-column
     kernel's (same column code) and within the parity rule of the oracle."""
     import torch
     from conftest import env_context
@@ -526,7 +526,7 @@ def test_tiled_shallow_kernel_matches_thread_per_column(n, pad, variant, strict)
     ld = n + pad
     o = P.KernelOptions(variant=variant, strict=strict)
     got = []
-    for env in ({"CVG_SHALLOW_TILE": "2"}, {"CVG_SHALLOW_TILE": "0"}):
+    for env in ({"CVG_SHALLOW_TILE": "2"}, {"CVG_SHALLOW_TILE": "0"}, {"CVG_SHALLOW_TILE": "2", "CVG_TILE_TMA": "0"}):
         c = env_context(**env)
         ds = torch.from_numpy(s).to(dev)
         Tb = torch.zeros((L, ld), dtype=torch.float64, device=dev)
@@ -541,11 +541,12 @@ def test_tiled_shallow_kernel_matches_thread_per_column(n, pad, variant, strict)
         c.check()
         got.append([P.ColumnOutputs(*[t.cpu().numpy() for t in oo]) for oo in outs])
         c.close()
-    for a, b in zip(got[0], got[1]):
-        for f in ("tend_T", "tend_q", "precip", "work_units", "exited_early"):
-            x, y = getattr(a, f), getattr(b, f)
-            assert np.array_equal(x.view(np.int64) if x.dtype == np.float64 else x,
-                                  y.view(np.int64) if y.dtype == np.float64 else y), f
+    for other in got[1:]:   # TMA tiles == thread-per-column == cp.async tiles
+        for a, b in zip(got[0], other):
+            for f in ("tend_T", "tend_q", "precip", "work_units", "exited_early"):
+                x, y = getattr(a, f), getattr(b, f)
+                assert np.array_equal(x.view(np.int64) if x.dtype == np.float64 else x,
+                                      y.view(np.int64) if y.dtype == np.float64 else y), f
     oo = O.Options(variant=variant)
     both_close(got[0][0], O.convection("deep", s, T, q, oo))
     both_close(got[0][1], O.convection("shallow", s, T, q, oo))
