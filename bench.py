@@ -575,6 +575,9 @@ def run_gpu_arm(args):
                           "bound": "fp64" if t_flop >= t_hbm else "hbm",
                           "roofline_ms": 1e3 * t_roof, "frac": 1e3 * t_roof / (ms_total / K),
                           "frac_fp64_model": 1e3 * t_flop / (ms_total / K), "frac_hbm": 1e3 * t_hbm / (ms_total / K),
+                          # the north star's nominal 8 TB/s beside the measured copy bandwidth (both)
+                          "frac_hbm_nominal_8tbs": 1e3 * (bytes_job / nper / 8.0e12) / (ms_total / K),
+                          "achieved_hbm_gbs": bytes_job / nper / (ms_total / K * 1e-3) / 1e9,
                           "traffic": step_traffic,
                           "note": "job FLOPs and bytes over all ranks / N GPUs; frac = roofline time / max-over-ranks step time; "
                                   "traffic = ncu DRAM bytes of one step, range capture with the kernels overlapped (profiles/deep_traffic.json, N=1 only)"},
