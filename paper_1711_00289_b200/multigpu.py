@@ -26,7 +26,7 @@ BYTES_PER_COLUMN_30 = 1482.0
 # Measured per-unit step times on one B200 at L = 30 (the analogue of the
 # reference's calibrate(), hetero.cpp:110-163), refit whenever the kernels
 # change (tools/fit_partition.py: c4, c5_50 and c5_05 ranges of 1/2/4/8-way
-# balanced and naive splits, each a whole step, least squares): t = 31 us +
+# balanced and naive splits, each a whole step, least squares): t = 35 us +
 # 0.86 ns per triggered column + 0.154 ns per column -- a triggered column
 # weighs ~5.6 plain columns (profiles/r04_fit_partition.json, tiled shallow kernel).
 MEASURED_NS_PER_TRIGGERED = float(os.environ.get("CVG_W_TRIGGERED", 0.86))   # (overrides: calibration runs)

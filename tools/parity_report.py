@@ -2,7 +2,7 @@
 """GPU parity report: every BASELINE config at its stated size, every variant,
 every device path, EVERY column against the CPU oracle (test infrastructure).
 
-    python tools/parity_report.py --out profiles/parity_r04.json [--quick]
+    python tools/parity_report.py --out profiles/parity_r05.json [--quick]
 
 Per (config, variant, path) and kernel it records, for tend_T / tend_q /
 precip, the worst absolute and relative deviation and the number of values
