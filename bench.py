@@ -513,6 +513,9 @@ def run_gpu_arm(args):
         e2e = {"value": n_total * Ke / el, "unit": UNIT, "h2d_bytes_per_step": int(tb[0]),
                "d2h_bytes_per_step": int(tb[1]), "steps": Ke,
                "ms_per_step": 1e3 * el / Ke,
+               # the last step's copies and kernels on rank 0 (cvg_stats; summed over the pipeline's chunks,
+               # which overlap, so the three add up to more than the step)
+               "split_ms": {"h2d": float(stt.h2d_ms), "d2h": float(stt.d2h_ms), "kernels": float(stt.device_ms)},
                "note": "cvg_convect (C ABI) on pinned host SoA buffers: H2D inputs, compute, D2H all outputs, per step; wall clock, max over ranks"}
         for a in pin + pdo + pso:
             a.free()
@@ -595,10 +598,22 @@ def run_gpu_arm(args):
         "clocks": clk.summary(),
     }
     if rank == 0:
+        # the reference's pinned BenchRecord CSV (bench.hpp:30-43): one run-gpu
+        # row per run, by default into the scratch directory gpurun_out/
+        rec_path = None
+        if args.records == "auto" and not args.slice:
+            rec_path = os.path.join(ROOT, "gpurun_out", "run_gpu_records.csv")
+        elif args.records not in (None, "auto", "none"):
+            rec_path = args.records
+        if rec_path:
+            try:
+                from paper_1711_00289_b200 import records
+                os.makedirs(os.path.dirname(os.path.abspath(rec_path)), exist_ok=True)
+                records.append_records(rec_path, [records.run_gpu_record(line)])
+                line["records"] = os.path.relpath(rec_path, ROOT)
+            except OSError as e:   # a read-only tree: the JSON line is the result
+                line["records"] = f"not written ({e.__class__.__name__})"
         print(json.dumps(line), flush=True)
-        if args.records:   # the reference's pinned BenchRecord CSV (bench.hpp:30-43)
-            from paper_1711_00289_b200 import records
-            records.append_records(args.records, [records.run_gpu_record(line)])
     ctx.close()
     if dist:
         dist.barrier()
@@ -619,8 +634,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-loop", action="store_true", help="skip the feedback-loop measurement")
-    ap.add_argument("--records", default=None,
-                    help="append a run-gpu BenchRecord row (reference CSV schema) to this file")
+    ap.add_argument("--records", default="auto",
+                    help="append a run-gpu BenchRecord row (reference CSV schema) to this file "
+                         "(default: gpurun_out/run_gpu_records.csv; 'none' to skip)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slice", default=None,
                     help="diagnostic R/W: time rank R's share of a W-way partition alone on one GPU")
