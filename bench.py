@@ -513,9 +513,11 @@ def run_gpu_arm(args):
         e2e = {"value": n_total * Ke / el, "unit": UNIT, "h2d_bytes_per_step": int(tb[0]),
                "d2h_bytes_per_step": int(tb[1]), "steps": Ke,
                "ms_per_step": 1e3 * el / Ke,
-               # the last step's copies and kernels on rank 0 (cvg_stats; summed over the pipeline's chunks,
-               # which overlap, so the three add up to more than the step)
-               "split_ms": {"h2d": float(stt.h2d_ms), "d2h": float(stt.d2h_ms), "kernels": float(stt.device_ms)},
+               # the last step on rank 0 (cvg_stats): copy times summed over the pipeline's chunks (they
+               # overlap one another and the kernels, so they add up to more than the step) and the span
+               # from the first chunk's first kernel to the last chunk's last (CUDA events)
+               "split_ms": {"h2d_sum": float(stt.h2d_ms), "d2h_sum": float(stt.d2h_ms),
+                            "device_span": float(stt.device_ms)},
                "note": "cvg_convect (C ABI) on pinned host SoA buffers: H2D inputs, compute, D2H all outputs, per step; wall clock, max over ranks"}
         for a in pin + pdo + pso:
             a.free()
